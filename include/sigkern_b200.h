@@ -1,0 +1,170 @@
+/*
+ * sigkern_b200 — C ABI of the B200-native truncated signature-kernel Gram path.
+ *
+ * This is the drop-in boundary for the reference's dual dynamic-programming
+ * path, `sigkern.kernels.sig_kernel_gram(..., algorithm="dp")`
+ * (/root/reference/pkg/src/sigkern/kernels.py:530-600), and the two public
+ * building blocks it is made of, `increment_tensor` (kernels.py:263-281) and
+ * `sig_levels_dp` (kernels.py:144-201).
+ *
+ * Conventions
+ *  - Every array pointer is DEVICE memory owned by the caller; every call is
+ *    stream-ordered on `stream` (a cudaStream_t, NULL = legacy default stream).
+ *  - Sequence batches are row-major float64 (N, L, d), exactly the reference's
+ *    `(N, L, d)` ndarray layout (kernels.py:414-422).
+ *  - Kernel values are float64 on output, as in the reference.
+ *  - The only scratch is the caller-sized workspace (`sk_workspace_bytes`);
+ *    the library never allocates device memory itself.
+ *  - Return value: SK_OK or an SK_ERR_* code; `sk_last_error()` holds a
+ *    thread-local message. Argument validation mirrors the reference's
+ *    ValueError cases; the host wrapper re-raises them with the reference's
+ *    exception types and messages.
+ *  - Re-entrant per stream; no global mutable state besides the error text.
+ */
+#ifndef SIGKERN_B200_H
+#define SIGKERN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SK_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define SK_API __attribute__((visibility("default")))
+#else
+#define SK_API
+#endif
+
+enum sk_status {
+  SK_OK = 0,
+  SK_ERR_INVALID = 1,     /* bad argument (reference: ValueError) */
+  SK_ERR_CUDA = 2,        /* CUDA runtime / launch failure */
+  SK_ERR_WORKSPACE = 3,   /* workspace too small */
+  SK_ERR_UNSUPPORTED = 4  /* configuration outside the compiled kernels */
+};
+
+/* Static kernel kinds, in the order of static/kernels.py:25-33. */
+enum sk_static_kind {
+  SK_LINEAR = 0,
+  SK_POLYNOMIAL = 1,
+  SK_RBF = 2,
+  SK_MATERN12 = 3,
+  SK_MATERN32 = 4,
+  SK_MATERN52 = 5,
+  SK_RATIONAL_QUADRATIC = 6
+};
+
+/* KernelConfig.normalization (kernels.py:52). */
+enum sk_normalization { SK_NORM_NONE = 0, SK_NORM_LEVELWISE = 1, SK_NORM_GLOBAL = 2 };
+
+/* Arithmetic of the level recursion. FP32: the fused sm_100a kernels
+ * (float32 increments and scans, float64 cross-lane level sums); FP64:
+ * float64 throughout (bit-level agreement with the reference to ~1e-13). */
+enum sk_precision { SK_PREC_FP32 = 0, SK_PREC_FP64 = 1 };
+
+/* StaticKernelSpec (static/kernels.py:39-53). */
+typedef struct sk_static_spec {
+  int32_t kind;       /* sk_static_kind */
+  int32_t degree;     /* polynomial degree */
+  double scale;       /* linear/polynomial inner-product scale */
+  double gamma;       /* polynomial offset */
+  double bandwidth;   /* length scale of the stationary kinds */
+  double alpha;       /* rational-quadratic shape */
+} sk_static_spec;
+
+/* KernelConfig (kernels.py:59-91). `order` is the EFFECTIVE order
+ * (KernelConfig.effective_order, kernels.py:85-91): 1 <= order <= max(1, n_levels). */
+typedef struct sk_kernel_config {
+  sk_static_spec static_spec;
+  int32_t n_levels;
+  int32_t order;
+  int32_t difference;     /* 1: double-differenced increments, 0: raw point kernel */
+  int32_t normalization;  /* sk_normalization */
+  int32_t precision;      /* sk_precision */
+  int32_t reserved;       /* must be 0 */
+} sk_kernel_config;
+
+/* Library ABI version (SK_ABI_VERSION). */
+SK_API int sk_abi_version(void);
+
+/* Thread-local text of the last error on this host thread ("" if none). */
+SK_API const char *sk_last_error(void);
+
+/* Bytes of workspace `sk_gram` / `sk_self_levels` need for these shapes
+ * (0 when the float64 path is selected). `ny`/`ly` may be 0 for self levels. */
+SK_API size_t sk_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int64_t d,
+                          const sk_kernel_config *cfg);
+
+/* 1 if `cfg` at these shapes runs on the fused FP32 sm_100a kernels, 0 if it
+ * runs on the general float64 kernel. */
+SK_API int sk_fast_path(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config *cfg);
+
+/*
+ * Self level values k_m(x_i, x_i), m = 0..n_levels, for every sequence:
+ * out is (n, n_levels+1) float64.  Replaces the diagonal pass of
+ * sig_kernel_gram (kernels.py:589-595).  Computed with the same kernel and
+ * the same arithmetic as the diagonal of `sk_gram`, so normalised diagonals
+ * are exactly 1.
+ */
+SK_API int sk_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
+                   const sk_kernel_config *cfg, double *out,
+                   void *workspace, size_t workspace_bytes, void *stream);
+
+/*
+ * Signature-kernel Gram block (kernels.py:530-600, algorithm="dp").
+ *
+ *  X (nx, lx, d), Y (ny, ly, d). symmetric=1 means Y is X (K(X) in the
+ *  reference, `Y=None`): only pairs with i <= j are evaluated and K[i,j] is
+ *  mirrored into K[j,i] bit for bit (kernels.py:449-468); Y/ny/ly are ignored.
+ *
+ *  Rows [row_begin, row_end) of X are evaluated (multi-GPU row sharding):
+ *   - cross (symmetric=0): K points at the storage of row `row_begin`;
+ *     K[(i-row_begin)*ldk + j].
+ *   - symmetric: K points at row 0 of the full (nx, nx) matrix; pairs
+ *     (i, j>=i) with i in the row range are written at [i,j] and [j,i].
+ *  levels (optional, may be NULL): per-pair level values, laid out like K but
+ *   with (n_levels+1) float64 per entry (row stride ldk*(n_levels+1)).
+ *  diag_x (nx, M+1) / diag_y (ny, M+1): self levels from sk_self_levels,
+ *   required when normalization != SK_NORM_NONE. For SK_NORM_GLOBAL the
+ *   caller has already rejected non-positive self kernels (kernels.py:519-527).
+ *  K may be NULL if only `levels` is wanted.
+ */
+SK_API int sk_gram(const double *X, int64_t nx, int64_t lx,
+            const double *Y, int64_t ny, int64_t ly, int64_t d,
+            int32_t symmetric, const sk_kernel_config *cfg,
+            int64_t row_begin, int64_t row_end,
+            const double *diag_x, const double *diag_y,
+            double *K, int64_t ldk, double *levels,
+            void *workspace, size_t workspace_bytes, void *stream);
+
+/*
+ * Level values from given increment matrices (sig_levels_dp, kernels.py:144-201):
+ *  A is (batch, t1, t2) float64, or (n_levels, batch, t1, t2) when
+ *  per_level=1 (level m consumes A[m-1], kernels.py:129-141).
+ *  out is (batch, n_levels+1) float64.  Float64 arithmetic.
+ */
+SK_API size_t sk_levels_dp_workspace_bytes(int64_t batch, int64_t t1, int64_t t2,
+                                    int32_t n_levels, int32_t order);
+SK_API int sk_levels_dp(const double *A, int64_t batch, int64_t t1, int64_t t2,
+                 int32_t n_levels, int32_t order, int32_t per_level,
+                 double *out, void *workspace, size_t workspace_bytes, void *stream);
+
+/*
+ * Increment matrices (increment_tensor, kernels.py:263-281), float64:
+ *  paired=0: all pairs, out (nx, ny, T1, T2); paired=1: nx == ny, out (nx, T1, T2),
+ *  with T = l-1 when difference=1 (0 if l < 2) and T = l otherwise.
+ */
+SK_API int sk_increment_tensor(const double *X, int64_t nx, int64_t lx,
+                        const double *Y, int64_t ny, int64_t ly, int64_t d,
+                        int32_t paired, const sk_static_spec *spec, int32_t difference,
+                        double *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SIGKERN_B200_H */

@@ -1,0 +1,177 @@
+// C ABI of libsigkern_b200 (include/sigkern_b200.h): validation and dispatch
+// between the fused FP32 kernels and the general float64 kernel.
+#include <algorithm>
+#include <string>
+
+#include "sk_common.cuh"
+
+namespace sk {
+
+namespace {
+thread_local std::string g_error;
+}
+
+void set_error(const std::string &msg) { g_error = msg; }
+void clear_error() { g_error.clear(); }
+
+int sm_count() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+namespace {
+
+int check_config(const sk_kernel_config *c) {
+  if (!c) return fail(SK_ERR_INVALID, "config is NULL");
+  const sk_static_spec &s = c->static_spec;
+  if (s.kind < SK_LINEAR || s.kind > SK_RATIONAL_QUADRATIC)
+    return fail(SK_ERR_INVALID, "unknown kernel kind " + std::to_string(s.kind));
+  if (!(s.scale > 0)) return fail(SK_ERR_INVALID, "scale must be positive");
+  if (s.degree < 1) return fail(SK_ERR_INVALID, "degree must be a positive integer");
+  if (!(s.bandwidth > 0)) return fail(SK_ERR_INVALID, "bandwidth must be positive");
+  if (!(s.alpha > 0)) return fail(SK_ERR_INVALID, "alpha must be positive");
+  if (c->n_levels < 0) return fail(SK_ERR_INVALID, "n_levels must be a non-negative integer");
+  if (c->order < 1 || c->order > std::max(1, c->n_levels))
+    return fail(SK_ERR_INVALID, "order must be the effective order in [1, max(1, n_levels)]");
+  if (c->normalization < SK_NORM_NONE || c->normalization > SK_NORM_GLOBAL)
+    return fail(SK_ERR_INVALID, "normalization must be none/levelwise/global");
+  if (c->precision != SK_PREC_FP32 && c->precision != SK_PREC_FP64)
+    return fail(SK_ERR_INVALID, "precision must be SK_PREC_FP32 or SK_PREC_FP64");
+  if (c->reserved != 0) return fail(SK_ERR_INVALID, "reserved must be 0");
+  return SK_OK;
+}
+
+int check_generic_limits(const sk_kernel_config &c) {
+  if (c.n_levels > GEN_MAX_LEVELS)
+    return fail(SK_ERR_UNSUPPORTED, "n_levels > " + std::to_string(GEN_MAX_LEVELS) +
+                                        " is not compiled into the float64 kernel");
+  if (c.order > GEN_MAX_ORDER)
+    return fail(SK_ERR_UNSUPPORTED, "order > " + std::to_string(GEN_MAX_ORDER) +
+                                        " is not compiled into the float64 kernel");
+  return SK_OK;
+}
+
+int check_batch(const double *X, int64_t n, int64_t l, int64_t d, const char *what) {
+  if (n < 0 || l < 1 || d < 1)
+    return fail(SK_ERR_INVALID, std::string(what) + ": expected an (N, L, d) batch with L, d >= 1");
+  if (n > 0 && !X) return fail(SK_ERR_INVALID, std::string(what) + " is NULL");
+  return SK_OK;
+}
+
+}  // namespace
+}  // namespace sk
+
+using namespace sk;
+
+extern "C" {
+
+int sk_abi_version(void) { return SK_ABI_VERSION; }
+
+const char *sk_last_error(void) { return g_error.c_str(); }
+
+int sk_fast_path(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config *cfg) {
+  if (!cfg) return 0;
+  return fast_supported(lx, ly, d, *cfg) ? 1 : 0;
+}
+
+size_t sk_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int64_t d,
+                          const sk_kernel_config *cfg) {
+  if (!cfg) return 0;
+  size_t need = fast_workspace_bytes(nx, lx, ny, ly, d, *cfg);
+  // float64 path: self levels of X and Y, and the Gram itself
+  if (!fast_supported(lx, lx, d, *cfg)) need = std::max(need, generic_workspace_bytes(nx, lx, lx, *cfg));
+  if (ny > 0) {
+    if (!fast_supported(ly, ly, d, *cfg))
+      need = std::max(need, generic_workspace_bytes(ny, ly, ly, *cfg));
+    if (!fast_supported(lx, ly, d, *cfg))
+      need = std::max(need, generic_workspace_bytes(nx * ny, lx, ly, *cfg));
+  }
+  return need;
+}
+
+int sk_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
+                   const sk_kernel_config *cfg, double *out, void *workspace,
+                   size_t workspace_bytes, void *stream) {
+  clear_error();
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  if ((rc = check_batch(X, n, l, d, "X"))) return rc;
+  if (n > 0 && !out) return fail(SK_ERR_INVALID, "out is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (fast_supported(l, l, d, *cfg))
+    return fast_self_levels(X, n, l, d, *cfg, out, workspace, workspace_bytes, st);
+  if ((rc = check_generic_limits(*cfg))) return rc;
+  return generic_self_levels(X, n, l, d, *cfg, out, workspace, workspace_bytes, st);
+}
+
+int sk_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny, int64_t ly,
+            int64_t d, int32_t symmetric, const sk_kernel_config *cfg, int64_t row_begin,
+            int64_t row_end, const double *diag_x, const double *diag_y, double *K,
+            int64_t ldk, double *levels, void *workspace, size_t workspace_bytes,
+            void *stream) {
+  clear_error();
+  int rc = check_config(cfg);
+  if (rc) return rc;
+  if ((rc = check_batch(X, nx, lx, d, "X"))) return rc;
+  if (symmetric) {
+    Y = X;
+    ny = nx;
+    ly = lx;
+  } else if ((rc = check_batch(Y, ny, ly, d, "Y"))) {
+    return rc;
+  }
+  if (row_begin < 0 || row_end > nx || row_begin > row_end)
+    return fail(SK_ERR_INVALID, "row range outside [0, nx]");
+  if (!K && !levels) return fail(SK_ERR_INVALID, "neither K nor levels requested");
+  if (ldk < ny) return fail(SK_ERR_INVALID, "ldk < ny");
+  if (cfg->normalization != SK_NORM_NONE && (!diag_x || (!symmetric && !diag_y)))
+    return fail(SK_ERR_INVALID, "normalization needs diag_x and diag_y self levels");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (fast_supported(lx, ly, d, *cfg))
+    return fast_gram(X, nx, lx, Y, ny, ly, d, symmetric, *cfg, row_begin, row_end, diag_x,
+                     symmetric ? diag_x : diag_y, K, ldk, levels, workspace, workspace_bytes,
+                     st);
+  if ((rc = check_generic_limits(*cfg))) return rc;
+  return generic_gram(X, nx, lx, Y, ny, ly, d, symmetric, *cfg, row_begin, row_end, diag_x,
+                      symmetric ? diag_x : diag_y, K, ldk, levels, workspace, workspace_bytes,
+                      st);
+}
+
+size_t sk_levels_dp_workspace_bytes(int64_t batch, int64_t t1, int64_t t2, int32_t n_levels,
+                                    int32_t order) {
+  (void)t1;
+  return generic_levels_dp_workspace_bytes(batch, t2, n_levels, order);
+}
+
+int sk_levels_dp(const double *A, int64_t batch, int64_t t1, int64_t t2, int32_t n_levels,
+                 int32_t order, int32_t per_level, double *out, void *workspace,
+                 size_t workspace_bytes, void *stream) {
+  clear_error();
+  if (batch < 0 || t1 < 0 || t2 < 0) return fail(SK_ERR_INVALID, "negative shape");
+  if (n_levels < 0) return fail(SK_ERR_INVALID, "n_levels must be a non-negative integer");
+  if (order < 1) return fail(SK_ERR_INVALID, "order must be a positive integer");
+  if (n_levels > GEN_MAX_LEVELS)
+    return fail(SK_ERR_UNSUPPORTED, "n_levels > " + std::to_string(GEN_MAX_LEVELS));
+  if (std::min(order, std::max(n_levels, 1)) > GEN_MAX_ORDER)
+    return fail(SK_ERR_UNSUPPORTED, "order > " + std::to_string(GEN_MAX_ORDER));
+  if (batch > 0 && (!out || (!A && t1 * t2 > 0))) return fail(SK_ERR_INVALID, "NULL pointer");
+  return generic_levels_from_increments(A, batch, t1, t2, n_levels, order, per_level, out,
+                                        workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int sk_increment_tensor(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
+                        int64_t ly, int64_t d, int32_t paired, const sk_static_spec *spec,
+                        int32_t difference, double *out, void *stream) {
+  clear_error();
+  if (!spec) return fail(SK_ERR_INVALID, "spec is NULL");
+  int rc;
+  if ((rc = check_batch(X, nx, lx, d, "X"))) return rc;
+  if ((rc = check_batch(Y, ny, ly, d, "Y"))) return rc;
+  if (paired && nx != ny) return fail(SK_ERR_INVALID, "paired increments need nx == ny");
+  return increment_tensor(X, nx, lx, Y, ny, ly, d, paired, *spec, difference, out,
+                          (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,170 @@
+// Shared definitions for the sigkern_b200 CUDA library (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/sigkern_b200.h"
+
+namespace sk {
+
+// Thread-local error text behind sk_last_error().
+void set_error(const std::string &msg);
+void clear_error();
+
+#define SK_CHECK_CUDA(expr)                                                        \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess) {                                                       \
+      ::sk::set_error(std::string("CUDA error: ") + cudaGetErrorString(_e) +       \
+                      " at " __FILE__ ":" + std::to_string(__LINE__));             \
+      return SK_ERR_CUDA;                                                          \
+    }                                                                              \
+  } while (0)
+
+#define SK_CHECK_LAUNCH() SK_CHECK_CUDA(cudaGetLastError())
+
+inline int fail(int code, const std::string &msg) {
+  set_error(msg);
+  return code;
+}
+
+// Number of SMs of the current device (cached per device).
+int sm_count();
+
+// ---------------------------------------------------------------------------
+// float64 static kernels: static/kernels.py:68-89 (norm-expansion squared
+// distance as in kernels.py:256-259 and static/kernels.py:108-114).
+// ---------------------------------------------------------------------------
+struct StaticF64 {
+  int kind;
+  int degree;
+  double scale, gamma, bandwidth, alpha;
+};
+
+__host__ __device__ inline StaticF64 to_static(const sk_static_spec &s) {
+  StaticF64 r;
+  r.kind = s.kind;
+  r.degree = s.degree;
+  r.scale = s.scale;
+  r.gamma = s.gamma;
+  r.bandwidth = s.bandwidth;
+  r.alpha = s.alpha;
+  return r;
+}
+
+__device__ inline double ipow(double b, int e) {
+  double r = 1.0;
+  for (int k = 0; k < e; ++k) r *= b;
+  return r;
+}
+
+// k(x, y) for two points (stride-1 coordinates).
+__device__ inline double static_eval_f64(const StaticF64 &S, const double *x, const double *y,
+                                         int d) {
+  double xy = 0.0;
+  for (int k = 0; k < d; ++k) xy = fma(x[k], y[k], xy);
+  if (S.kind == SK_LINEAR) return S.scale * xy;
+  if (S.kind == SK_POLYNOMIAL) return pow(S.scale * xy + S.gamma, (double)S.degree);
+  double xx = 0.0, yy = 0.0;
+  for (int k = 0; k < d; ++k) {
+    xx = fma(x[k], x[k], xx);
+    yy = fma(y[k], y[k], yy);
+  }
+  double sq = xx + yy - 2.0 * xy;
+  if (sq < 0.0) sq = 0.0;
+  const double bw2 = S.bandwidth * S.bandwidth;
+  switch (S.kind) {
+    case SK_RBF:
+      return exp(sq / (-2.0 * bw2));
+    case SK_RATIONAL_QUADRATIC:
+      return pow(1.0 + sq / (2.0 * S.alpha * bw2), -S.alpha);
+    case SK_MATERN12:
+      return exp(-(sqrt(sq) / S.bandwidth));
+    case SK_MATERN32: {
+      const double sr = 1.7320508075688772 * (sqrt(sq) / S.bandwidth);
+      return (1.0 + sr) * exp(-sr);
+    }
+    case SK_MATERN52: {
+      const double r = sqrt(sq) / S.bandwidth;
+      const double sr = 2.23606797749979 * r;
+      return (1.0 + sr + (5.0 / 3.0) * r * r) * exp(-sr);
+    }
+    default:
+      return 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Level-sum epilogue: kernels.py:586-600 (+ _normalize_levelwise 510-516,
+// _normalize_global 519-527). lv[0..M] are the pair's level values.
+// ---------------------------------------------------------------------------
+__device__ inline double finish_entry(const double *lv, int M, int norm, const double *dx,
+                                      const double *dy) {
+  if (norm == SK_NORM_LEVELWISE) {
+    double acc = 0.0;
+    for (int m = 0; m <= M; ++m) {
+      const double a = dx[m] > 0.0 ? dx[m] : 0.0;
+      const double b = dy[m] > 0.0 ? dy[m] : 0.0;
+      const double den = sqrt(a * b);
+      if (den > 0.0) acc += lv[m] / den;
+    }
+    return acc / (double)(M + 1);
+  }
+  double tot = 0.0;
+  for (int m = 0; m <= M; ++m) tot += lv[m];
+  if (norm == SK_NORM_GLOBAL) {
+    double sx = 0.0, sy = 0.0;
+    for (int m = 0; m <= M; ++m) {
+      sx += dx[m];
+      sy += dy[m];
+    }
+    return tot / sqrt(sx * sy);
+  }
+  return tot;
+}
+
+// ---------------------------------------------------------------------------
+// Entry points of the individual translation units.
+// ---------------------------------------------------------------------------
+
+// Generic float64 path (any M <= GEN_MAX_LEVELS, p <= GEN_MAX_ORDER, kind, difference).
+constexpr int GEN_MAX_LEVELS = 16;
+constexpr int GEN_MAX_ORDER = 8;
+
+size_t generic_workspace_bytes(int64_t npairs, int64_t lx, int64_t ly, const sk_kernel_config &c);
+
+int generic_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
+                 int64_t ly, int64_t d, int symmetric, const sk_kernel_config &c,
+                 int64_t row_begin, int64_t row_end, const double *diag_x,
+                 const double *diag_y, double *K, int64_t ldk, double *levels, void *ws,
+                 size_t ws_bytes, cudaStream_t st);
+
+int generic_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
+                        const sk_kernel_config &c, double *out, void *ws, size_t ws_bytes,
+                        cudaStream_t st);
+
+size_t generic_levels_dp_workspace_bytes(int64_t batch, int64_t t2, int M, int p);
+int generic_levels_from_increments(const double *A, int64_t batch, int64_t t1, int64_t t2,
+                                   int M, int p, int per_level, double *out, void *ws,
+                                   size_t ws_bytes, cudaStream_t st);
+
+int increment_tensor(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
+                     int64_t ly, int64_t d, int paired, const sk_static_spec &sp,
+                     int difference, double *out, cudaStream_t st);
+
+// Fused FP32 path.
+bool fast_supported(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c);
+size_t fast_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int64_t d,
+                            const sk_kernel_config &c);
+int fast_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
+              int64_t ly, int64_t d, int symmetric, const sk_kernel_config &c,
+              int64_t row_begin, int64_t row_end, const double *diag_x, const double *diag_y,
+              double *K, int64_t ldk, double *levels, void *ws, size_t ws_bytes,
+              cudaStream_t st);
+int fast_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
+                     const sk_kernel_config &c, double *out, void *ws, size_t ws_bytes,
+                     cudaStream_t st);
+
+}  // namespace sk

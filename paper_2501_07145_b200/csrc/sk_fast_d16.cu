@@ -1,0 +1,10 @@
+// Fused FP32 kernels instantiated for 16 padded channels (n_levels 1..8, rbf/linear).
+#include "sk_fast.cuh"
+
+namespace sk {
+namespace fast {
+int launch_d16(const Params &P, int M, int linear, size_t smem, cudaStream_t st) {
+  return launch_impl<16>(P, M, linear, smem, st);
+}
+}  // namespace fast
+}  // namespace sk

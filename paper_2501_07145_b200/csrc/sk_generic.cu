@@ -1,0 +1,389 @@
+// General float64 path: any static kind, any order p <= GEN_MAX_ORDER, any
+// n_levels <= GEN_MAX_LEVELS, difference on/off, per-level increment lists.
+//
+// One thread owns one sequence pair and sweeps its T1 x T2 increment grid row
+// by row, carrying only column accumulators (O(T2) state) instead of the
+// reference's full (p, p, T1, T2) state tensors (kernels.py:175-199). The
+// recursion is exactly the reference's (kernels.py:179-199):
+//   R'[0,0] = A * S(C),            C = sum_{q,r} R[q,r], S = 2-D exclusive prefix
+//   R'[q,0] = A/(q+1) * E_j(sum_r R[q-1,r])
+//   R'[0,q] = A/(q+1) * E_i(sum_q' R[q',q-1])
+//   R'[q,r] = A/((q+1)(r+1)) * R[q-1,r-1]
+// evaluated cell by cell: S(C)(i,j) is a running row sum of the column
+// accumulators colC(j) = sum_{i'<i} C(i',j); E_j is a running row sum; E_i is
+// a column accumulator. Per-thread column state lives in the workspace with
+// the pair index fastest, so a warp's accesses are coalesced.
+//
+// This path is the float64 (bit-level) reference-parity path and the
+// fallback for configurations the fused FP32 kernels do not instantiate.
+
+#include <algorithm>
+#include <cstdio>
+
+#include "sk_common.cuh"
+
+namespace sk {
+
+namespace {
+
+constexpr int GEN_THREADS = 128;
+
+struct GenParams {
+  // point inputs (mode 0..2) or increment input (mode 3)
+  const double *X;
+  const double *Y;
+  const double *A;
+  int64_t nx, lx, ny, ly, d;
+  int64_t t1, t2;  // increment grid
+  StaticF64 S;
+  int M, p, difference, per_level;
+  int mode;  // 0 rect pairs, 1 symmetric (j >= i), 2 paired (i == j), 3 increments
+  int64_t row_begin;
+  int64_t g0, count;  // pair ids [g0, g0+count) of this chunk
+  double *scratch;    // [slot][count]
+  double *lv;         // [count][M+1]
+};
+
+__device__ inline void pair_of(const GenParams &P, int64_t g, int64_t &i, int64_t &j) {
+  if (P.mode == 2 || P.mode == 3) {
+    i = g;
+    j = g;
+  } else {
+    i = P.row_begin + g / P.ny;
+    j = g % P.ny;
+  }
+}
+
+__global__ void __launch_bounds__(GEN_THREADS) generic_levels_kernel(GenParams P) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= P.count) return;
+  const int64_t g = P.g0 + t;
+  int64_t i, j;
+  pair_of(P, g, i, j);
+  const int M = P.M;
+  double *out = P.lv + t * (M + 1);
+  out[0] = 1.0;
+  for (int m = 1; m <= M; ++m) out[m] = 0.0;
+  if (P.mode == 1 && j < i) return;  // lower triangle of a symmetric Gram is mirrored
+  const int64_t T1 = P.t1, T2 = P.t2;
+  if (M == 0 || T1 <= 0 || T2 <= 0) return;
+  const int p = P.p;
+  const int64_t CH = P.count;
+
+  // workspace slots: colC[(m-1)*T2 + j] m=1..M-1, colSY[((m-1)*(p-1)+r)*T2 + j], Gprev[ly]
+  double *colC = P.scratch + t;
+  double *colSY = colC + (int64_t)(M - 1) * T2 * CH;
+  double *Gprev = colSY + (int64_t)(M - 1) * (p - 1) * T2 * CH;
+  for (int64_t k = 0; k < (int64_t)(M - 1) * T2 * p; ++k) colC[k * CH] = 0.0;
+
+  const double *xs = nullptr, *ys = nullptr;
+  const bool from_points = P.mode != 3;
+  if (from_points) {
+    xs = P.X + i * P.lx * P.d;
+    ys = (P.mode == 2 ? P.X : P.Y) + j * P.ly * P.d;
+    if (P.difference)
+      for (int64_t c = 0; c < P.ly; ++c) Gprev[c * CH] = static_eval_f64(P.S, xs, ys + c * P.d, (int)P.d);
+  }
+
+  double s2d[GEN_MAX_LEVELS];
+  double ex[GEN_MAX_LEVELS * GEN_MAX_ORDER];
+  double Ra[GEN_MAX_ORDER * GEN_MAX_ORDER], Rb[GEN_MAX_ORDER * GEN_MAX_ORDER];
+  double lsum[GEN_MAX_LEVELS + 1];
+  for (int m = 0; m <= M; ++m) lsum[m] = 0.0;
+
+  for (int64_t r = 0; r < T1; ++r) {
+    for (int m = 0; m < M; ++m) s2d[m] = 0.0;
+    for (int k = 0; k < M * p; ++k) ex[k] = 0.0;
+    const double *xa = nullptr;
+    double gl = 0.0;  // G(r+1, c) of the previous column
+    if (from_points && P.difference) {
+      xa = xs + (r + 1) * P.d;
+      gl = static_eval_f64(P.S, xa, ys, (int)P.d);
+    }
+    for (int64_t c = 0; c < T2; ++c) {
+      double a_shared = 0.0;
+      if (from_points) {
+        if (P.difference) {
+          // kernels.py:281: G[1:,1:] - G[:-1,1:] - G[1:,:-1] + G[:-1,:-1]
+          const double g11 = static_eval_f64(P.S, xa, ys + (c + 1) * P.d, (int)P.d);
+          const double g01 = Gprev[(c + 1) * CH];
+          const double g00 = Gprev[c * CH];
+          a_shared = g11 - g01 - gl + g00;
+          Gprev[c * CH] = gl;
+          if (c == T2 - 1) Gprev[(c + 1) * CH] = g11;
+          gl = g11;
+        } else {
+          a_shared = static_eval_f64(P.S, xs + r * P.d, ys + c * P.d, (int)P.d);
+        }
+      } else if (!P.per_level) {
+        a_shared = P.A[(g * T1 + r) * T2 + c];
+      }
+      double *Rp = Ra, *Rc = Rb;  // Rp: level m-1 at this cell, Rc: level m
+      for (int m = 1; m <= M; ++m) {
+        const double am =
+            (from_points || !P.per_level) ? a_shared
+                                          : P.A[(((int64_t)(m - 1) * P.count + g) * T1 + r) * T2 + c];
+        for (int k = 0; k < p * p; ++k) Rc[k] = 0.0;
+        if (m == 1) {
+          Rc[0] = am;
+        } else {
+          const int mm = m - 2;  // index of level m-1 in the accumulators
+          double Ctot = 0.0;
+          for (int k = 0; k < p * p; ++k) Ctot += Rp[k];
+          double *cc = colC + ((int64_t)mm * T2 + c) * CH;
+          const double old = *cc;
+          const double S2 = s2d[mm];
+          s2d[mm] += old;
+          *cc = old + Ctot;
+          Rc[0] = am * S2;
+          for (int q = 1; q < p; ++q) {
+            double sx = 0.0, sy = 0.0;
+            for (int r2 = 0; r2 < p; ++r2) sx += Rp[(q - 1) * p + r2];
+            for (int q2 = 0; q2 < p; ++q2) sy += Rp[q2 * p + (q - 1)];
+            double &e = ex[mm * p + (q - 1)];
+            const double E = e;
+            e += sx;
+            double *cy = colSY + (((int64_t)mm * (p - 1) + (q - 1)) * T2 + c) * CH;
+            const double oldy = *cy;
+            *cy = oldy + sy;
+            Rc[q * p] = (am / (q + 1)) * E;
+            Rc[q] = (am / (q + 1)) * oldy;
+          }
+          for (int q = 1; q < p; ++q)
+            for (int r2 = 1; r2 < p; ++r2)
+              Rc[q * p + r2] = (am / ((q + 1) * (r2 + 1))) * Rp[(q - 1) * p + (r2 - 1)];
+        }
+        double cs = 0.0;
+        for (int k = 0; k < p * p; ++k) cs += Rc[k];
+        lsum[m] += cs;
+        double *tmp = Rp;
+        Rp = Rc;
+        Rc = tmp;
+      }
+    }
+  }
+  for (int m = 1; m <= M; ++m) out[m] = lsum[m];
+}
+
+// Normalisation / level-sum epilogue for a chunk of pairs (kernels.py:586-600).
+__global__ void generic_finish_kernel(GenParams P, int norm, const double *diag_x,
+                                      const double *diag_y, double *K, int64_t ldk,
+                                      double *levels) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= P.count) return;
+  int64_t i, j;
+  pair_of(P, P.g0 + t, i, j);
+  if (P.mode == 1 && j < i) return;
+  const int M = P.M;
+  const double *lv = P.lv + t * (M + 1);
+  const bool sym = P.mode == 1;
+  const int64_t row = sym ? i : i - P.row_begin;
+  if (levels) {
+    for (int m = 0; m <= M; ++m) levels[(row * ldk + j) * (M + 1) + m] = lv[m];
+    if (sym && j != i)
+      for (int m = 0; m <= M; ++m) levels[(j * ldk + i) * (M + 1) + m] = lv[m];
+  }
+  if (K) {
+    const double v = finish_entry(lv, M, norm, diag_x ? diag_x + i * (M + 1) : nullptr,
+                                  diag_y ? diag_y + j * (M + 1) : nullptr);
+    K[row * ldk + j] = v;
+    if (sym && j != i) K[j * ldk + i] = v;
+  }
+}
+
+__global__ void copy_levels_kernel(const double *lv, int64_t count, int M, double *out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < count * (M + 1)) out[t] = lv[t];
+}
+
+int64_t scratch_slots(int64_t t2, int64_t ly, int M, int p) {
+  const int64_t mm = std::max(M - 1, 0);
+  return mm * t2 * p + ly + 1;
+}
+
+int64_t chunk_pairs(int64_t npairs, int64_t slots, int M) {
+  const int64_t per = (slots + M + 1) * 8;
+  const int64_t budget = 256ll << 20;
+  int64_t ch = std::max<int64_t>(1024, budget / per);
+  ch = std::min<int64_t>(ch, 1 << 16);
+  return std::max<int64_t>(1, std::min(ch, npairs));
+}
+
+int run_chunks(GenParams P, int64_t npairs, int norm, const double *diag_x,
+               const double *diag_y, double *K, int64_t ldk, double *levels, double *self_out,
+               void *ws, size_t ws_bytes, cudaStream_t st) {
+  const int64_t slots = scratch_slots(P.t2, P.ly, P.M, P.p);
+  const int64_t ch = chunk_pairs(npairs, slots, P.M);
+  const size_t need = (size_t)ch * (slots + P.M + 1) * sizeof(double);
+  if (ws_bytes < need || ws == nullptr)
+    return fail(SK_ERR_WORKSPACE, "workspace too small for the float64 path: need " +
+                                      std::to_string(need) + " bytes");
+  P.scratch = (double *)ws;
+  P.lv = P.scratch + ch * slots;
+  for (int64_t g0 = 0; g0 < npairs; g0 += ch) {
+    P.g0 = g0;
+    P.count = std::min(ch, npairs - g0);
+    const int blocks = (int)((P.count + GEN_THREADS - 1) / GEN_THREADS);
+    generic_levels_kernel<<<blocks, GEN_THREADS, 0, st>>>(P);
+    SK_CHECK_LAUNCH();
+    if (self_out) {
+      const int64_t n = P.count * (P.M + 1);
+      copy_levels_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+          P.lv, P.count, P.M, self_out + g0 * (P.M + 1));
+    } else {
+      generic_finish_kernel<<<blocks, GEN_THREADS, 0, st>>>(P, norm, diag_x, diag_y, K, ldk,
+                                                           levels);
+    }
+    SK_CHECK_LAUNCH();
+  }
+  return SK_OK;
+}
+
+GenParams base_params(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
+                      int64_t ly, int64_t d, const sk_kernel_config &c) {
+  GenParams P{};
+  P.X = X;
+  P.Y = Y;
+  P.nx = nx;
+  P.lx = lx;
+  P.ny = ny;
+  P.ly = ly;
+  P.d = d;
+  P.S = to_static(c.static_spec);
+  P.M = c.n_levels;
+  P.p = std::max(1, std::min(c.order, std::max(c.n_levels, 1)));
+  P.difference = c.difference;
+  P.t1 = c.difference ? std::max<int64_t>(lx - 1, 0) : lx;
+  P.t2 = c.difference ? std::max<int64_t>(ly - 1, 0) : ly;
+  return P;
+}
+
+}  // namespace
+
+size_t generic_workspace_bytes(int64_t npairs, int64_t lx, int64_t ly, const sk_kernel_config &c) {
+  const int M = c.n_levels;
+  const int p = std::max(1, std::min(c.order, std::max(M, 1)));
+  const int64_t t2 = c.difference ? std::max<int64_t>(ly - 1, 0) : ly;
+  const int64_t slots = scratch_slots(t2, ly, M, p);
+  const int64_t ch = chunk_pairs(std::max<int64_t>(npairs, 1), slots, M);
+  (void)lx;
+  return (size_t)ch * (slots + M + 1) * sizeof(double);
+}
+
+int generic_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
+                 int64_t ly, int64_t d, int symmetric, const sk_kernel_config &c,
+                 int64_t row_begin, int64_t row_end, const double *diag_x,
+                 const double *diag_y, double *K, int64_t ldk, double *levels, void *ws,
+                 size_t ws_bytes, cudaStream_t st) {
+  if (symmetric) {
+    Y = X;
+    ny = nx;
+    ly = lx;
+  }
+  GenParams P = base_params(X, nx, lx, Y, ny, ly, d, c);
+  P.mode = symmetric ? 1 : 0;
+  P.row_begin = row_begin;
+  const int64_t npairs = (row_end - row_begin) * ny;
+  if (npairs <= 0) return SK_OK;
+  return run_chunks(P, npairs, c.normalization, diag_x, diag_y, K, ldk, levels, nullptr, ws,
+                    ws_bytes, st);
+}
+
+int generic_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
+                        const sk_kernel_config &c, double *out, void *ws, size_t ws_bytes,
+                        cudaStream_t st) {
+  GenParams P = base_params(X, n, l, X, n, l, d, c);
+  P.mode = 2;
+  if (n <= 0) return SK_OK;
+  return run_chunks(P, n, SK_NORM_NONE, nullptr, nullptr, nullptr, 0, nullptr, out, ws,
+                    ws_bytes, st);
+}
+
+size_t generic_levels_dp_workspace_bytes(int64_t batch, int64_t t2, int M, int p) {
+  p = std::max(1, std::min(p, std::max(M, 1)));
+  return (size_t)std::max<int64_t>(batch, 1) * (scratch_slots(t2, 0, M, p) + M + 1) *
+         sizeof(double);
+}
+
+int generic_levels_from_increments(const double *A, int64_t batch, int64_t t1, int64_t t2,
+                                   int M, int p, int per_level, double *out, void *ws,
+                                   size_t ws_bytes, cudaStream_t st) {
+  if (batch <= 0) return SK_OK;
+  GenParams P{};
+  P.A = A;
+  P.M = M;
+  P.p = std::max(1, std::min(p, std::max(M, 1)));
+  P.per_level = per_level;
+  P.mode = 3;
+  P.t1 = t1;
+  P.t2 = t2;
+  P.ly = 0;
+  P.nx = P.ny = batch;
+  P.difference = 1;
+  // the per-level layout indexes A with the full batch, so the batch is one chunk
+  const size_t need = generic_levels_dp_workspace_bytes(batch, t2, M, P.p);
+  if (ws == nullptr || ws_bytes < need)
+    return fail(SK_ERR_WORKSPACE, "workspace too small for sk_levels_dp: need " +
+                                      std::to_string(need) + " bytes");
+  const int64_t slots = scratch_slots(t2, 0, M, P.p);
+  P.scratch = (double *)ws;
+  P.lv = P.scratch + batch * slots;
+  P.g0 = 0;
+  P.count = batch;
+  const int blocks = (int)((batch + GEN_THREADS - 1) / GEN_THREADS);
+  generic_levels_kernel<<<blocks, GEN_THREADS, 0, st>>>(P);
+  SK_CHECK_LAUNCH();
+  const int64_t n = batch * (M + 1);
+  copy_levels_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(P.lv, batch, M, out);
+  SK_CHECK_LAUNCH();
+  return SK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// increment_tensor (kernels.py:263-281), float64.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void increment_kernel(const double *X, int64_t nx, int64_t lx, const double *Y,
+                                 int64_t ny, int64_t ly, int64_t d, int paired, StaticF64 S,
+                                 int difference, int64_t t1, int64_t t2, double *out) {
+  const int64_t npairs = paired ? nx : nx * ny;
+  const int64_t total = npairs * t1 * t2;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e % t2;
+    const int64_t r = (e / t2) % t1;
+    const int64_t g = e / (t1 * t2);
+    const int64_t i = paired ? g : g / ny;
+    const int64_t j = paired ? g : g % ny;
+    const double *xs = X + i * lx * d;
+    const double *ys = Y + j * ly * d;
+    double v;
+    if (difference) {
+      const double g11 = static_eval_f64(S, xs + (r + 1) * d, ys + (c + 1) * d, (int)d);
+      const double g01 = static_eval_f64(S, xs + r * d, ys + (c + 1) * d, (int)d);
+      const double g10 = static_eval_f64(S, xs + (r + 1) * d, ys + c * d, (int)d);
+      const double g00 = static_eval_f64(S, xs + r * d, ys + c * d, (int)d);
+      v = g11 - g01 - g10 + g00;
+    } else {
+      v = static_eval_f64(S, xs + r * d, ys + c * d, (int)d);
+    }
+    out[e] = v;
+  }
+}
+}  // namespace
+
+int increment_tensor(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
+                     int64_t ly, int64_t d, int paired, const sk_static_spec &sp,
+                     int difference, double *out, cudaStream_t st) {
+  const int64_t t1 = difference ? std::max<int64_t>(lx - 1, 0) : lx;
+  const int64_t t2 = difference ? std::max<int64_t>(ly - 1, 0) : ly;
+  const int64_t total = (paired ? nx : nx * ny) * t1 * t2;
+  if (total <= 0) return SK_OK;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 32);
+  increment_kernel<<<(unsigned)blocks, 256, 0, st>>>(X, nx, lx, Y, ny, ly, d, paired,
+                                                     to_static(sp), difference, t1, t2, out);
+  SK_CHECK_LAUNCH();
+  return SK_OK;
+}
+
+}  // namespace sk

@@ -1,0 +1,81 @@
+"""C-ABI library: loads without a GPU, exports every symbol the header declares,
+and its host-side logic (validation, fast-path selection, workspace sizing)."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+from paper_2501_07145_b200 import KernelConfig, StaticKernelSpec, _native
+
+HEADER = os.path.join(ROOT, "include", "sigkern_b200.h")
+
+
+def _declared():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"SK_API\s+(?:const\s+char\s*\*|int|size_t)\s*(sk_\w+)\s*\(", text)))
+
+
+def test_library_loads_and_exports_header_symbols():
+    lib = _native.load()
+    names = _declared()
+    assert names, "no SK_API declarations parsed"
+    assert set(names) == set(_native.EXPORTS)
+    for n in names:
+        assert hasattr(lib, n), n
+    assert lib.sk_abi_version() == 1
+    assert lib.sk_last_error() == b""
+
+
+def _cfg(**kw):
+    st = kw.pop("static", StaticKernelSpec(kind="rbf"))
+    return _native.config_struct(KernelConfig(static=st, **kw), kw.pop("precision", "fp32"))
+
+
+def test_fast_path_selection():
+    lib = _native.load()
+    c3 = _native.config_struct(KernelConfig(n_levels=5, order=1, normalization="levelwise"))
+    assert lib.sk_fast_path(256, 256, 16, c3) == 1          # c3
+    assert lib.sk_fast_path(50, 50, 3, c3) == 1             # c1 shapes
+    lin = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="linear"), n_levels=3))
+    assert lib.sk_fast_path(128, 128, 16, lin) == 1
+    assert lib.sk_fast_path(128, 128, 128, lin) == 0        # d > 16: float64 path (for now)
+    geo = _native.config_struct(KernelConfig(n_levels=5, order=5))
+    assert lib.sk_fast_path(128, 128, 8, geo) == 0          # p > 1
+    f64 = _native.config_struct(KernelConfig(n_levels=5), "fp64")
+    assert lib.sk_fast_path(256, 256, 16, f64) == 0
+    mat = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="matern32")))
+    assert lib.sk_fast_path(64, 64, 4, mat) == 0
+    assert lib.sk_fast_path(300, 300, 4, c3) == 0           # more columns than one warp holds
+    assert lib.sk_fast_path(2, 256, 4, c3) == 0             # x shorter than the wavefront
+
+
+def test_workspace_sizes():
+    lib = _native.load()
+    c3 = _native.config_struct(KernelConfig(n_levels=5, normalization="levelwise"))
+    n, L, d = 8192, 256, 16
+    ws = lib.sk_workspace_bytes(n, L, n, L, d, c3)
+    # packed fp32 X (x role) + Y (y role, 20 floats per point)
+    assert ws == 2 * n * L * 20 * 4
+    f64 = _native.config_struct(KernelConfig(n_levels=3, order=2), "fp64")
+    assert lib.sk_workspace_bytes(4, 6, 5, 7, 2, f64) > 0
+
+
+def test_invalid_arguments_rejected_before_device_work():
+    lib = _native.load()
+    bad = _native.config_struct(KernelConfig(n_levels=3))
+    bad.order = 9  # effective order must be <= n_levels
+    rc = lib.sk_gram(None, 0, 5, None, 0, 5, 2, 0, ctypes.byref(bad), 0, 0, None, None,
+                     None, 0, None, None, 0, None)
+    assert rc == _native.SK_ERR_INVALID
+    assert b"order" in lib.sk_last_error()
+    good = _native.config_struct(KernelConfig(n_levels=3, normalization="levelwise"))
+    rc = lib.sk_gram(None, 0, 5, None, 0, 5, 2, 0, ctypes.byref(good), 0, 0, None, None,
+                     None, 0, None, None, 0, None)
+    assert rc == _native.SK_ERR_INVALID  # neither K nor levels
+    rc = lib.sk_levels_dp(None, 1, 2, 2, 17, 1, 0, None, None, 0, None)
+    assert rc == _native.SK_ERR_UNSUPPORTED
+    with pytest.raises(ValueError):
+        _native.check(_native.SK_ERR_INVALID, "x")

@@ -1,0 +1,174 @@
+"""Parity of the CUDA path with the reference (golden vectors) and the CPU oracle.
+
+Tolerances (north star): max elementwise relative error vs float64 <= 1e-5 for
+normalised kernels, <= 1e-4 unnormalised, for the FP32 path; the float64 path
+is held to the reference's own 1e-10.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import oracle_static, pkg_config
+from oracle import sigkern_oracle as O
+from paper_2501_07145_b200 import (KernelConfig, SeedStream, StaticKernelSpec, gen_brownian,
+                                   increment_tensor, sig_kernel_gram, sig_levels_dp,
+                                   uses_fast_path)
+
+pytestmark = pytest.mark.gpu
+
+TOL_NORM, TOL_RAW = 1e-5, 1e-4
+
+
+def _rel(K, R):
+    K = np.asarray(K)
+    R = np.asarray(R)
+    err = np.abs(K - R) / np.maximum(np.abs(R), 1e-300)
+    err[(K == 0) & (R == 0)] = 0.0
+    return float(err.max()) if err.size else 0.0
+
+
+def test_library_kernels_launch():
+    X = gen_brownian(4, 10, 2, SeedStream(3)).data
+    K = sig_kernel_gram(X, cfg=KernelConfig(n_levels=3))
+    assert K.shape == (4, 4) and np.isfinite(K).all()
+
+
+def test_golden_cases_fp64(gram_cases):
+    for name, X, Y, c, K_ref in gram_cases:
+        if name in ("bench_c5", "bench_c5n", "bench_c4"):
+            continue  # float64 thread-per-pair at L=2048 / d=128 is slow; FP32 path below
+        K = sig_kernel_gram(X, Y, cfg=pkg_config(c), precision="fp64")
+        assert K.shape == K_ref.shape, name
+        # Matern kinds take sqrt of the norm-expansion squared distance, which
+        # amplifies summation-order rounding near x = y (different from BLAS);
+        # everything else is held to the reference's own 1e-10.
+        rtol = 1e-8 if c["kind"].startswith("matern") else 1e-10
+        assert np.allclose(K, K_ref, rtol=rtol, atol=1e-12), (name, _rel(K, K_ref))
+
+
+def test_golden_cases_fp32(gram_cases):
+    n_fast = 0
+    for name, X, Y, c, K_ref in gram_cases:
+        cfg = pkg_config(c)
+        K = sig_kernel_gram(X, Y, cfg=cfg)
+        ly = X.shape[1] if Y is None else Y.shape[1]
+        n_fast += uses_fast_path(X.shape[1], ly, X.shape[2], cfg)
+        tol = TOL_RAW if c["normalization"] == "none" else TOL_NORM
+        # tiny random cases can have entries that cancel to ~0; judge those absolutely
+        scale = np.maximum(np.abs(K_ref), 1e-3 * np.abs(K_ref).max())
+        err = float((np.abs(K - K_ref) / scale).max())
+        assert err <= tol, (name, err)
+    assert n_fast >= 20  # the fused kernels really ran on most cases
+
+
+@pytest.mark.parametrize("name", ["bench_c1", "bench_c2", "bench_c2n", "bench_c3", "bench_c3u",
+                                  "bench_c4", "bench_c5", "bench_c5n"])
+def test_bench_config_blocks(gram_cases, name):
+    """BASELINE configs (sub-blocks) vs the reference at the north-star tolerances."""
+    _, X, Y, c, K_ref = gram_cases.get(name)
+    K = sig_kernel_gram(X, Y, cfg=pkg_config(c))
+    tol = TOL_RAW if c["normalization"] == "none" else TOL_NORM
+    assert _rel(K, K_ref) <= tol, _rel(K, K_ref)
+
+
+def test_symmetric_bitwise_and_unit_diagonal():
+    X = gen_brownian(40, 50, 3, SeedStream(1)).data
+    for norm in ("levelwise", "global"):
+        K = sig_kernel_gram(X, cfg=KernelConfig(n_levels=5, normalization=norm))
+        assert np.array_equal(K, K.T)
+        assert np.array_equal(np.diag(K), np.ones(40)), norm
+
+
+def test_symmetric_equals_cross_entries():
+    X = gen_brownian(20, 30, 4, SeedStream(9)).data
+    cfg = KernelConfig(n_levels=4)
+    Ks = sig_kernel_gram(X, cfg=cfg)
+    Kc = sig_kernel_gram(X, X, cfg=cfg)
+    iu = np.triu_indices(20)
+    assert np.array_equal(Ks[iu], Kc[iu])  # same roles (row = streamed x) on the upper triangle
+
+
+def test_deterministic():
+    X = gen_brownian(64, 64, 8, SeedStream(2)).data
+    Y = gen_brownian(48, 64, 8, SeedStream(3)).data
+    cfg = KernelConfig(n_levels=5, normalization="levelwise")
+    assert np.array_equal(sig_kernel_gram(X, Y, cfg=cfg), sig_kernel_gram(X, Y, cfg=cfg))
+
+
+def test_row_blocks_compose():
+    from paper_2501_07145_b200.kernels import gram_block
+    X = torch.from_numpy(gen_brownian(70, 40, 5, SeedStream(4)).data).cuda()
+    Y = torch.from_numpy(gen_brownian(33, 40, 5, SeedStream(5)).data).cuda()
+    cfg = KernelConfig(n_levels=4, normalization="levelwise")
+    full, _ = gram_block(X, Y, cfg)
+    parts = [gram_block(X, Y, cfg, r0, r1)[0] for r0, r1 in ((0, 23), (23, 50), (50, 70))]
+    assert torch.equal(torch.cat(parts), full)
+    Ks = torch.zeros((70, 70), dtype=torch.float64, device="cuda")
+    for r0, r1 in ((0, 10), (10, 40), (40, 70)):
+        gram_block(X, None, cfg, r0, r1, K=Ks)
+    assert torch.equal(Ks, gram_block(X, None, cfg)[0])
+
+
+def test_fp32_vs_fp64_c3_shapes():
+    X = gen_brownian(12, 256, 16, SeedStream(1)).data
+    Y = gen_brownian(10, 256, 16, SeedStream(2)).data
+    for norm, tol in (("levelwise", TOL_NORM), ("none", TOL_RAW)):
+        cfg = KernelConfig(n_levels=5, normalization=norm)
+        assert uses_fast_path(256, 256, 16, cfg)
+        K32 = sig_kernel_gram(X, Y, cfg=cfg)
+        K64 = sig_kernel_gram(X, Y, cfg=cfg, precision="fp64")
+        assert _rel(K32, K64) <= tol
+
+
+def test_ragged_lengths_and_short_sequences():
+    X = gen_brownian(5, 33, 3, SeedStream(6)).data
+    Y = gen_brownian(4, 70, 3, SeedStream(7)).data
+    cfg = KernelConfig(n_levels=4, normalization="levelwise")
+    R = O.gram(X, Y, M=4, p=1, normalization="levelwise")
+    assert _rel(sig_kernel_gram(X, Y, cfg=cfg), R) <= TOL_NORM
+    assert _rel(sig_kernel_gram(Y, X, cfg=cfg), R.T) <= TOL_NORM
+    Z = np.random.default_rng(0).standard_normal((3, 1, 3))  # one point: no increments
+    K = sig_kernel_gram(Z, X, cfg=KernelConfig(n_levels=3))
+    assert np.array_equal(K, np.ones((3, 5)))
+
+
+def test_levels_dp_golden(levels_golden):
+    z = levels_golden
+    for t in range(24):
+        A = z[f"dp{t}__A"]
+        M, p = (int(v) for v in z[f"dp{t}__Mp"])
+        assert np.allclose(sig_levels_dp(A, M, order=p), z[f"dp{t}__dp"], rtol=1e-10, atol=1e-12)
+    mats = list(z["perlevel__A"])
+    assert np.allclose(sig_levels_dp(mats, 3, order=2), z["perlevel__dp"], rtol=1e-10)
+    assert np.allclose(sig_levels_dp(z["batched__A"], 4, order=2), z["batched__dp"], rtol=1e-10)
+
+
+def test_increment_tensor_golden(levels_golden):
+    z = levels_golden
+    for kind in O.KINDS:
+        spec = StaticKernelSpec(kind=kind, bandwidth=1.2)
+        x, y = z[f"inc_{kind}__x"], z[f"inc_{kind}__y"]
+        assert np.allclose(increment_tensor(spec, x, y), z[f"inc_{kind}__A"], atol=1e-12)
+        assert np.allclose(increment_tensor(spec, x, y, difference=False), z[f"inc_{kind}__G"],
+                           atol=1e-12)
+
+
+def test_torch_tensors_stay_on_device():
+    X = torch.from_numpy(gen_brownian(8, 20, 3, SeedStream(8)).data).cuda()
+    K = sig_kernel_gram(X, cfg=KernelConfig(n_levels=3, normalization="levelwise"))
+    assert isinstance(K, torch.Tensor) and K.is_cuda and K.shape == (8, 8)
+
+
+def test_full_c3_prefix_block(gram_cases):
+    """Full-size c3 cross Gram is out of the oracle's reach; its top-left block
+    must equal the golden 4x4 block (inputs are prefix-stable), and all
+    entries of a normalised Gram lie in [-1, 1] up to rounding."""
+    _, X4, Y4, c, K_ref = gram_cases.get("bench_c3")
+    n = 1024
+    X = gen_brownian(n, 256, 16, SeedStream(1)).data
+    Y = gen_brownian(n, 256, 16, SeedStream(2)).data
+    assert np.array_equal(X[:4], X4) and np.array_equal(Y[:4], Y4)
+    K = sig_kernel_gram(X, Y, cfg=pkg_config(c))
+    assert _rel(K[:4, :4], K_ref) <= TOL_NORM
+    assert np.isfinite(K).all() and np.abs(K).max() <= 1.0 + 1e-6

@@ -1,0 +1,78 @@
+"""Pin the CPU oracle (oracle/sigkern_oracle.py) against the reference's own outputs.
+
+The golden vectors were produced by running the reference itself
+(tests/golden/make_golden.py). CPU only.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import oracle_static
+from oracle import sigkern_oracle as O
+
+
+def test_gen_brownian_bitwise(brownian_golden):
+    for key in ("n3_L10_d5_s1", "n2_L256_d16_s1", "n2_L256_d16_s2", "n1_L2_d1_s7"):
+        n, L, d, s = [int(t[1:]) for t in key.split("_")]
+        assert np.array_equal(O.gen_brownian(n, L, d, s), brownian_golden[key]), key
+    assert np.array_equal(O.gen_brownian(2, 12, 2, 31, ("a", "b")), brownian_golden["child_path"])
+
+
+def test_gen_brownian_window_stable():
+    full = O.gen_brownian(6, 9, 3, 4)
+    assert np.array_equal(O.gen_brownian(3, 9, 3, 4, start=2), full[2:5])
+
+
+def test_gram_cases_match_reference(gram_cases):
+    worst = 0.0
+    for name, X, Y, c, K_ref in gram_cases:
+        if name.startswith("bench_c5") or name.startswith("bench_c4"):
+            continue  # large; covered by test_bench_blocks_match_reference
+        K = O.gram(X, Y, sp=oracle_static(c), M=c["n_levels"], p=c["order"],
+                   difference=c["difference"], normalization=c["normalization"])
+        assert K.shape == K_ref.shape
+        rel = np.abs(K - K_ref) / np.maximum(np.abs(K_ref), 1e-300)
+        worst = max(worst, float(rel.max()))
+        assert np.allclose(K, K_ref, rtol=1e-12, atol=1e-14), name
+    assert worst < 1e-12
+
+
+@pytest.mark.parametrize("name", ["bench_c4", "bench_c5"])
+def test_bench_blocks_match_reference(gram_cases, name):
+    _, X, Y, c, K_ref = gram_cases.get(name)
+    K = O.gram(X, Y, sp=oracle_static(c), M=c["n_levels"], p=c["order"],
+               normalization=c["normalization"])
+    assert np.array_equal(K, K_ref)
+
+
+def test_levels_dp_bitwise(levels_golden):
+    z = levels_golden
+    for t in range(24):
+        A = z[f"dp{t}__A"]
+        M, p = (int(v) for v in z[f"dp{t}__Mp"])
+        assert np.array_equal(O.levels_dp(A, M, p), z[f"dp{t}__dp"]), t
+        assert np.allclose(O.levels_bruteforce(A, M, p), z[f"dp{t}__bf"], rtol=1e-12, atol=1e-14)
+    mats = list(z["perlevel__A"])
+    assert np.array_equal(O.levels_dp(mats, 3, 2), z["perlevel__dp"])
+    assert np.array_equal(O.levels_dp(z["batched__A"], 4, 2), z["batched__dp"])
+
+
+def test_increments_bitwise(levels_golden):
+    z = levels_golden
+    for kind in O.KINDS:
+        sp = O.static_params(kind, bandwidth=1.2)
+        x, y = z[f"inc_{kind}__x"], z[f"inc_{kind}__y"]
+        assert np.array_equal(O.increments(sp, x, y), z[f"inc_{kind}__A"]), kind
+        assert np.array_equal(O.increments(sp, x, y, difference=False), z[f"inc_{kind}__G"]), kind
+
+
+def test_hand_values():
+    # test_acceptance.py:90-100: k1 = 6; k2 = 0 at p=1, 9 at p=2
+    lin = O.static_params("linear")
+    x = np.array([[0.0], [1.0], [3.0]])
+    y = np.array([[0.0], [2.0]])
+    A = O.increments(lin, x, y)
+    assert O.levels_dp(A, 2, 1)[1] == pytest.approx(6.0)
+    assert O.levels_dp(A, 2, 1)[2] == 0.0
+    assert O.levels_dp(A, 2, 2)[2] == pytest.approx(9.0)
+    assert O.levels_bruteforce(A, 2, 2)[2] == pytest.approx(9.0)
