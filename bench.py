@@ -1,0 +1,385 @@
+"""Benchmark: signature-kernel Gram entries/s and % of the FP32 roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl reference]
+
+Default workload (BASELINE.json configs[2], the metric's headline config):
+normalised (levelwise) order-1 RBF signature kernel, n_levels=5, cross Gram
+K(X, Y) of N = M' = 8192 random-walk sequences, L = 256, d = 16, float64
+inputs generated with the reference's own generator (restated bit for bit).
+
+A "step" is one whole Gram: self levels of X and Y (normalisation), the
+fused Gram kernel with its normalisation epilogue, and (N > 1) the NCCL
+all-gather of the row blocks. `value` is entries/s with inputs resident in
+HBM; `e2e` is the same through the public API (`SignatureKernel.__call__`)
+from pinned host float64 inputs to the host float64 Gram.
+"""
+
+from __future__ import annotations
+
+import os
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # the CPU baseline mirrors BASELINE.md
+
+import argparse
+import json
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "signature-kernel entries/sec and % FP32 roofline at L=256,d=16,m=5 (1/2/4/8 GPU)"
+
+# name: (N, L, d, n_levels, order, kind, normalization, symmetric, cpu sample k)
+CONFIGS = {
+    "c1": (64, 50, 3, 5, 1, "rbf", "levelwise", True, 64),
+    "c2": (1024, 128, 8, 5, 5, "rbf", "none", False, 12),
+    "c3": (8192, 256, 16, 5, 1, "rbf", "levelwise", False, 24),
+    "c4": (4096, 128, 128, 3, 1, "linear", "none", False, 16),
+    "c5": (512, 2048, 4, 8, 1, "rbf", "none", False, 2),
+}
+
+
+def flops_per_entry(L, d, M):
+    """North-star algorithmic work per Gram entry: 2 L L' (d + 2M)."""
+    return 2 * L * L * (d + 2 * M)
+
+
+def make_inputs(name):
+    from paper_2501_07145_b200 import SeedStream, gen_brownian
+    N, L, d = CONFIGS[name][:3]
+    X = gen_brownian(N, L, d, SeedStream(1)).data
+    Y = None if CONFIGS[name][7] else gen_brownian(N, L, d, SeedStream(2)).data
+    return X, Y
+
+
+def kernel_config(name):
+    from paper_2501_07145_b200 import KernelConfig, StaticKernelSpec
+    N, L, d, M, p, kind, norm, sym, _ = CONFIGS[name]
+    return KernelConfig(static=StaticKernelSpec(kind=kind), n_levels=M, order=p,
+                        normalization=norm)
+
+
+def workload(name):
+    N, L, d, M, p, kind, norm, sym, _ = CONFIGS[name]
+    return {"workload": f"{name}: SignatureKernel n_levels={M} order={p} {kind} "
+                        f"normalization={norm} {'K(X)' if sym else 'K(X,Y)'} N=M'={N} L={L} d={d}",
+            "N": N, "L": L, "d": d, "n_levels": M, "order": p, "static": f"{kind}(1.0)",
+            "normalization": norm, "symmetric": sym,
+            "l2": "no flush: packed inputs + float64 Gram exceed the 126 MB L2" if N >= 4096
+            else "small config (fits L2)"}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle port of the reference's algorithm; test infrastructure)
+# ---------------------------------------------------------------------------
+
+def cpu_sample(name, k=None, threads=None):
+    from oracle import sigkern_oracle as O
+    N, L, d, M, p, kind, norm, sym, kdef = CONFIGS[name]
+    k = k or kdef
+    threads = threads or O.host_threads()
+    X = O.gen_brownian(k, L, d, 1)
+    Y = None if sym else O.gen_brownian(k, L, d, 2)
+    sp = O.static_params(kind)
+    t0 = time.perf_counter()
+    O.gram(X, Y, sp=sp, M=M, p=p, normalization=norm, n_threads=threads)
+    dt = time.perf_counter() - t0
+    return k * k / dt, dt, k, threads
+
+
+def cpu_baseline_block(name):
+    rate, dt, k, threads = cpu_sample(name)
+    return {"value": rate, "unit": "entries/s", "cores": threads, "kind": "port",
+            "sample": f"{name} {k}x{k} sub-block ({k*k} entries) via oracle/sigkern_oracle.py "
+                      f"(numpy port of kernels.py:530-600), {dt:.2f} s, "
+                      f"OPENBLAS_NUM_THREADS=1, n_threads={threads}"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    name = args.config
+    for _ in range(args.warmup):
+        cpu_sample(name)
+    rates, times = [], []
+    for _ in range(args.steps):
+        r, dt, k, threads = cpu_sample(name)
+        rates.append(r)
+        times.append(dt)
+    value = float(np.median(rates))
+    line = {"metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(times)),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: gen_brownian random walks (SeedStream 1 / 2)",
+            "config": workload(name), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "entries/s", "cores": threads, "kind": "port",
+                             "sample": f"{name} {k}x{k} sub-block per step, oracle port of the "
+                                       f"reference's numpy DP, n_threads={threads}"},
+            "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            f = [t.strip() for t in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        load = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2501_07145_b200 import LinearKernel, RBFKernel, SignatureKernel
+    from paper_2501_07145_b200.distributed import row_blocks, sharded_gram, triangle_row_blocks
+    from paper_2501_07145_b200.kernels import _self_levels_t, gram_block
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    name = args.config
+    N, L, d, M, p, kind, norm, sym, _ = CONFIGS[name]
+    cfg = kernel_config(name)
+    Xh, Yh = make_inputs(name)
+    X = torch.from_numpy(Xh).to(dev)
+    Y = None if Yh is None else torch.from_numpy(Yh).to(dev)
+    ny = N
+
+    # one step: self levels (normalisation), fused Gram of this rank's rows, gather
+    gram_ms = []
+
+    def step(record=False):
+        ev = None
+        if world > 1:
+            def compute(Xt, Yt, c, r0, r1, prec, K_full):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                K, _ = gram_block(Xt, Yt, c, r0, r1, prec, K=K_full)
+                e1.record()
+                if record:
+                    gram_ms.append((e0, e1))
+                return K
+            return sharded_gram(X, Y, cfg, group=None, compute=compute)
+        diag_x = diag_y = None
+        if norm != "none":
+            diag_x = _self_levels_t(X, cfg, "fp32")
+            diag_y = diag_x if Y is None else _self_levels_t(Y, cfg, "fp32")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        K, _ = gram_block(X, Y, cfg, diag_x=diag_x, diag_y=diag_y)
+        e1.record()
+        if record:
+            gram_ms.append((e0, e1))
+        return K
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record()
+        for _ in range(args.steps):
+            K = step(record=True)
+        t1.record()
+        barrier()
+    elapsed = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([elapsed], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed = float(tt.item())
+    ms = elapsed / args.steps
+    entries = N * ny
+    value = entries / (ms / 1e3)
+
+    # dominant kernel: the fused Gram launch (sk_gram = 2 tiny pack kernels + Gram kernel)
+    g_ms = float(np.mean([a.elapsed_time(b) for a, b in gram_ms]))
+    if world > 1:
+        blocks = (triangle_row_blocks(N, world) if sym else row_blocks(N, world))[rank]
+        rows = blocks[1] - blocks[0]
+    else:
+        rows = N
+    if sym:
+        r0, r1 = (triangle_row_blocks(N, world)[rank] if world > 1 else (0, N))
+        pairs = sum(N - i for i in range(r0, r1))
+    else:
+        pairs = rows * ny
+    F = flops_per_entry(L, d, M)
+    achieved = pairs * F / (g_ms / 1e3) / 1e12
+    props = torch.cuda.get_device_properties(dev)
+    clocks = clk.summary()
+    sm_max = clocks["sm_max_mhz"] or 1965.0
+    peak = props.multi_processor_count * 128 * 2 * sm_max * 1e6 / 1e12
+
+    # end to end through the public API from pinned host buffers
+    e2e = None
+    if world == 1:
+        import torch as _t
+        Xp = _t.from_numpy(Xh).pin_memory()
+        Yp = None if Yh is None else _t.from_numpy(Yh).pin_memory()
+        Kh = _t.empty((N, ny), dtype=_t.float64).pin_memory()
+        static = RBFKernel(1.0) if kind == "rbf" else LinearKernel(1.0)
+        sk = SignatureKernel(n_levels=M, order=p, normalization=norm, static_kernel=static)
+
+        def e2e_step():
+            Xd = Xp.to(dev, non_blocking=True)
+            Yd = None if Yp is None else Yp.to(dev, non_blocking=True)
+            Kd = sk(Xd, Yd)
+            Kh.copy_(Kd, non_blocking=True)
+            return Kd
+
+        e2e_step()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        b.record()
+        torch.cuda.synchronize()
+        e_ms = a.elapsed_time(b) / args.e2e_steps
+        h2d = Xh.nbytes + (0 if Yh is None else Yh.nbytes)
+        e2e = {"value": entries / (e_ms / 1e3), "unit": "entries/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": N * ny * 8, "ms_per_step": e_ms,
+               "api": "SignatureKernel(...)(X, Y) on pinned host float64 -> host float64 K"}
+
+    launches_per_step = (2 if norm != "none" else 0) * (1 if sym else 2) + (2 if sym else 3)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "fp32 (float64 level sums and normalisation)",
+            "data": "synthetic: gen_brownian random walks, SeedStream(1)/(2), reference "
+                    "generator restated bit for bit",
+            "config": dict(workload(name), parallelism=f"rows{world}" if world > 1 else "single"),
+            "e2e": e2e,
+            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "sk::fast::gram_p1_kernel (fused Gram, per-launch CUDA events)",
+                         "flops_per_entry": F, "pairs_per_launch": pairs,
+                         "kernel_ms": g_ms,
+                         "peak_note": f"nominal FP32: {props.multi_processor_count} SMs x 128 "
+                                      f"lanes x 2 x {sm_max:.0f} MHz (no FP32 figure in "
+                                      f"MEASURED_PEAKS.json)"},
+            "cpu_baseline": cpu_baseline_block(name) if (world == 1 and not args.no_cpu) else None,
+            "clocks": clocks,
+            "gpu_launches": launches_per_step * args.steps,
+        }
+        if world == 1:
+            line["sample_check"] = sample_check(name, K, Xh, Yh)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def sample_check(name, K, Xh, Yh):
+    """Max relative error of a few Gram entries against the float64 oracle."""
+    from oracle import sigkern_oracle as O
+    N, L, d, M, p, kind, norm, sym, _ = CONFIGS[name]
+    idx = [(0, 0), (1, 5), (N - 1, N - 2), (N // 2, N // 3)]
+    Kc = K.cpu().numpy() if hasattr(K, "cpu") else np.asarray(K)
+    rows = sorted({i for i, _ in idx})
+    cols = sorted({j for _, j in idx})
+    Yref = Xh if Yh is None else Yh
+    R = O.gram(Xh[rows], Yref[cols], sp=O.static_params(kind), M=M, p=p, normalization=norm)
+    err = 0.0
+    for i, j in idx:
+        r = R[rows.index(i), cols.index(j)]
+        err = max(err, abs(Kc[i, j] - r) / abs(r))
+    return {"entries": idx, "max_rel_err": err}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--n", type=int, default=None,
+                    help="override N (profiling runs only; not a bench line)")
+    args = ap.parse_args()
+    if args.n:
+        c = list(CONFIGS[args.config])
+        c[0] = args.n
+        CONFIGS[args.config] = tuple(c)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -131,15 +131,127 @@ __device__ __forceinline__ void write_pair(const Params &P, int64_t i, int64_t j
   }
 }
 
+// Per-lane register state of one segment lane and the systolic step.
+template <int D, int M, bool LINEAR>
+struct LaneState {
+  static constexpr int DP = D + 4;
+  static constexpr int NCA = (M >= 2) ? M - 1 : 0;  // column-accumulated levels 1..M-1
+  static constexpr int NCR = (NCA > 0) ? NCA : 1;
+
+  float yv[C][D];
+  float yn[C];
+  float colacc[NCR][C];
+  float prevG[C];
+  float cout[NCR];
+  float kM, kout, lastD;
+
+  __device__ __forceinline__ void reset_pair() {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+#pragma unroll
+      for (int m = 0; m < NCR; ++m) colacc[m][c] = 0.f;
+    }
+    kM = 0.f;
+  }
+
+  // One row of this lane's C columns. KCHAIN: also run the level-M chain
+  // (only needed while some lane of the segment is at a pair boundary).
+  template <bool KCHAIN>
+  __device__ __forceinline__ void step(const float *__restrict__ xptr, int sw, bool first_lane) {
+    constexpr unsigned FULL = 0xffffffffu;
+    // (a) chain values produced by lane q-1 on the previous step
+    const float dl_raw = __shfl_up_sync(FULL, lastD, 1, sw);
+    float cin[NCR];
+#pragma unroll
+    for (int m = 0; m < NCA; ++m) {
+      const float v = __shfl_up_sync(FULL, cout[m], 1, sw);
+      cin[m] = first_lane ? 0.f : v;
+    }
+    if (KCHAIN) {
+      const float kin = __shfl_up_sync(FULL, kout, 1, sw);
+      kout = (first_lane ? 0.f : kin) + kM;  // complete at this lane's pair boundary
+    }
+
+    // (b) point-kernel row for this lane's columns
+    float g[C];
+    {
+      float acc[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[c] = yn[c];
+      const float4 *xr = reinterpret_cast<const float4 *>(xptr);
+#pragma unroll
+      for (int k4 = 0; k4 < D / 4; ++k4) {
+        const float4 xv = xr[k4];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          acc[c] = fmaf(xv.x, yv[c][4 * k4 + 0], acc[c]);
+          acc[c] = fmaf(xv.y, yv[c][4 * k4 + 1], acc[c]);
+          acc[c] = fmaf(xv.z, yv[c][4 * k4 + 2], acc[c]);
+          acc[c] = fmaf(xv.w, yv[c][4 * k4 + 3], acc[c]);
+        }
+      }
+      if (LINEAR) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) g[c] = acc[c];
+      } else {
+        const float xn = xptr[D];
+#pragma unroll
+        for (int c = 0; c < C; ++c) g[c] = ex2_approx(fminf(acc[c] + xn, 0.f));
+      }
+    }
+
+    // (c) increments of the previous DP row: A = D(g) - D(g-1), D = G(r,.) - G(r-1,.)
+    float a[C];
+    {
+      float dv[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        dv[c] = g[c] - prevG[c];
+        prevG[c] = g[c];
+      }
+      const float dl = first_lane ? dv[0] : dl_raw;  // column -1 does not exist: A = 0
+      a[0] = dv[0] - dl;
+#pragma unroll
+      for (int c = 1; c < C; ++c) a[c] = dv[c] - dv[c - 1];
+      lastD = dv[C - 1];
+    }
+
+    // (d) level recursion along the row (p = 1): R_m = A * S(R_{m-1})
+    if constexpr (M == 1) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) kM += a[c];
+    } else {
+      float sc[NCR];
+#pragma unroll
+      for (int m = 0; m < NCA; ++m) sc[m] = cin[m];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        float so[NCR];
+#pragma unroll
+        for (int m = 0; m < NCA; ++m) {
+          so[m] = sc[m];
+          sc[m] += colacc[m][c];
+        }
+        colacc[0][c] += a[c];
+#pragma unroll
+        for (int m = 1; m < NCA; ++m) colacc[m][c] = fmaf(a[c], so[m - 1], colacc[m][c]);
+        kM = fmaf(a[c], so[NCA - 1], kM);
+      }
+#pragma unroll
+      for (int m = 0; m < NCA; ++m) cout[m] = sc[m];
+    }
+  }
+};
+
 template <int D, int M, bool LINEAR>
 __global__ void __launch_bounds__(NTHREADS, 1) gram_p1_kernel(const Params P) {
   static_assert(D % 4 == 0, "D must be a multiple of 4");
   static_assert(M >= 1, "M >= 1");
-  constexpr int DP = D + 4;
-  constexpr int NCA = (M >= 2) ? M - 1 : 0;  // column-accumulated levels 1..M-1
-  constexpr int NCR = (NCA > 0) ? NCA : 1;
+  using LS = LaneState<D, M, LINEAR>;
+  constexpr int DP = LS::DP;
   extern __shared__ __align__(16) float smem[];
-  const int slot_floats = P.lx * DP;
+  const int lx = P.lx;
+  const int slot_floats = lx * DP;
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -148,8 +260,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) gram_p1_kernel(const Params P) {
   const int seg = warp * (32 / sw) + lane / sw;
   const bool last_lane = (q == sw - 1);
   const bool first_lane = (q == 0);
-  constexpr unsigned FULL = 0xffffffffu;
 
+  LS st;
   for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x) {
     const int64_t ty = tile % P.tiles_y;
     const int64_t tx = tile / P.tiles_y;
@@ -168,8 +280,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) gram_p1_kernel(const Params P) {
     const int64_t jj = jvalid ? j : P.ny - 1;
 
     // this lane's y columns (pre-scaled points and their n-terms)
-    float yv[C][D];
-    float yn[C];
     {
       const float *yp = P.ys + ((size_t)jj * P.lyp + (size_t)q * C) * DP;
 #pragma unroll
@@ -177,144 +287,50 @@ __global__ void __launch_bounds__(NTHREADS, 1) gram_p1_kernel(const Params P) {
 #pragma unroll
         for (int k4 = 0; k4 < D / 4; ++k4) {
           const float4 v = __ldg(reinterpret_cast<const float4 *>(yp + c * DP) + k4);
-          yv[c][4 * k4 + 0] = v.x;
-          yv[c][4 * k4 + 1] = v.y;
-          yv[c][4 * k4 + 2] = v.z;
-          yv[c][4 * k4 + 3] = v.w;
+          st.yv[c][4 * k4 + 0] = v.x;
+          st.yv[c][4 * k4 + 1] = v.y;
+          st.yv[c][4 * k4 + 2] = v.z;
+          st.yv[c][4 * k4 + 3] = v.w;
         }
-        yn[c] = LINEAR ? 0.f : __ldg(yp + c * DP + D);
+        st.yn[c] = LINEAR ? 0.f : __ldg(yp + c * DP + D);
+        st.prevG[c] = 0.f;
       }
     }
+    st.reset_pair();
+    st.kout = st.lastD = 0.f;
+#pragma unroll
+    for (int m = 0; m < LS::NCR; ++m) st.cout[m] = 0.f;
 
     __syncthreads();  // previous tile's readers are done with the ring
     stage_sequence(smem, P.xs + (size_t)x0 * P.lxp * DP, slot_floats);
 
-    float colacc[NCR][C];
-    float prevG[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      prevG[c] = 0.f;
-#pragma unroll
-      for (int m = 0; m < NCR; ++m) colacc[m][c] = 0.f;
-    }
-    float kM = 0.f, kout = 0.f, lastD = 0.f;
-    float cout[NCR];
-#pragma unroll
-    for (int m = 0; m < NCR; ++m) cout[m] = 0.f;
-
-    // lane q starts q steps late: until then it idles on rows of x_{x0}
-    int r = first_lane ? 0 : P.lx - q;
-    int job = first_lane ? 0 : -1;
-    const float *xptr = smem + r * DP;
-
+    // Epoch e streams x_{x0+e}: lane q starts that pair at step s = q (its
+    // row 0) and spends steps s < q finishing pair e-1. So pair boundaries
+    // only occur in steps s < sw ("phase A"); steps s >= sw are branch-free.
     for (int64_t e = 0; e <= njobs; ++e) {
       cp_async_wait_all();
       __syncthreads();
       if (e + 1 < njobs)
         stage_sequence(smem + ((e + 1) % NSLOT) * slot_floats,
                        P.xs + (size_t)(x0 + e + 1) * P.lxp * DP, slot_floats);
-      const int steps = (e < njobs) ? P.lx : sw;
-      for (int s = 0; s < steps; ++s) {
-        // (a) chain values produced by lane q-1 on the previous step
-        const float dl = __shfl_up_sync(FULL, lastD, 1, sw);
-        float cin[NCR];
-#pragma unroll
-        for (int m = 0; m < NCA; ++m) cin[m] = __shfl_up_sync(FULL, cout[m], 1, sw);
-        float kin = __shfl_up_sync(FULL, kout, 1, sw);
-        if (first_lane) {
-#pragma unroll
-          for (int m = 0; m < NCA; ++m) cin[m] = 0.f;
-          kin = 0.f;
+      const float *cur = smem + (e % NSLOT) * slot_floats;
+      // before its first pair a lane idles on rows of x_{x0} (slot 0)
+      const float *prev = (e == 0) ? smem : smem + ((e + NSLOT - 1) % NSLOT) * slot_floats;
+      const int steps = (e < njobs) ? lx : sw;
+      const int nA = min(sw, steps);
+      for (int s = 0; s < nA; ++s) {
+        const float *xp = (s < q) ? prev + (lx - q + s) * DP : cur + (s - q) * DP;
+        st.template step<true>(xp, sw, first_lane);
+        if (s == q) {  // this lane's pair boundary: pair e-1 is complete
+          if (last_lane && e >= 1 && jvalid) write_pair<M>(P, x0 + e - 1, j, st.cout, st.kout);
+          st.reset_pair();
         }
-        kout = kin + kM;  // level-M chain (complete at this lane's r == 0)
-
-        // (b) point-kernel row r for this lane's columns
-        float g[C];
-        {
-          float acc[C];
-#pragma unroll
-          for (int c = 0; c < C; ++c) acc[c] = yn[c];
-          const float4 *xr = reinterpret_cast<const float4 *>(xptr);
-#pragma unroll
-          for (int k4 = 0; k4 < D / 4; ++k4) {
-            const float4 xv = xr[k4];
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-              acc[c] = fmaf(xv.x, yv[c][4 * k4 + 0], acc[c]);
-              acc[c] = fmaf(xv.y, yv[c][4 * k4 + 1], acc[c]);
-              acc[c] = fmaf(xv.z, yv[c][4 * k4 + 2], acc[c]);
-              acc[c] = fmaf(xv.w, yv[c][4 * k4 + 3], acc[c]);
-            }
-          }
-          if (LINEAR) {
-#pragma unroll
-            for (int c = 0; c < C; ++c) g[c] = acc[c];
-          } else {
-            const float xn = xptr[D];
-#pragma unroll
-            for (int c = 0; c < C; ++c) g[c] = ex2_approx(fminf(acc[c] + xn, 0.f));
-          }
-        }
-
-        // (c) increments of DP row r-1: A = D(g) - D(g-1), D = G(r,.) - G(r-1,.)
-        float a[C];
-        {
-          float dv[C];
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            dv[c] = g[c] - prevG[c];
-            prevG[c] = g[c];
-          }
-          a[0] = dv[0] - (first_lane ? dv[0] : dl);
-#pragma unroll
-          for (int c = 1; c < C; ++c) a[c] = dv[c] - dv[c - 1];
-          lastD = dv[C - 1];
-        }
-
-        // (d) level recursion along the row (p = 1)
-        if constexpr (M == 1) {
-#pragma unroll
-          for (int c = 0; c < C; ++c) kM += a[c];
-        } else {
-          float sc[NCR];
-#pragma unroll
-          for (int m = 0; m < NCA; ++m) sc[m] = cin[m];
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            float so[NCR];
-#pragma unroll
-            for (int m = 0; m < NCA; ++m) {
-              so[m] = sc[m];
-              sc[m] += colacc[m][c];
-            }
-            colacc[0][c] += a[c];
-#pragma unroll
-            for (int m = 1; m < NCA; ++m) colacc[m][c] = fmaf(a[c], so[m - 1], colacc[m][c]);
-            kM = fmaf(a[c], so[NCA - 1], kM);
-          }
-#pragma unroll
-          for (int m = 0; m < NCA; ++m) cout[m] = sc[m];
-        }
-
-        // (e) pair boundary of this lane
-        if (r == 0) {
-          if (last_lane && job >= 1 && jvalid) write_pair<M>(P, x0 + job - 1, j, cout, kout);
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-#pragma unroll
-            for (int m = 0; m < NCR; ++m) colacc[m][c] = 0.f;
-          }
-          kM = 0.f;
-        }
-
-        // (f) advance
-        ++r;
-        xptr += DP;
-        if (r == P.lx) {
-          r = 0;
-          ++job;
-          xptr = smem + (job % NSLOT) * slot_floats;
-        }
+      }
+      const float *xp = cur + (nA - q) * DP;
+#pragma unroll 2
+      for (int s = nA; s < steps; ++s) {
+        st.template step<false>(xp, sw, first_lane);
+        xp += DP;
       }
     }
   }
