@@ -9,33 +9,22 @@ namespace fast {
 
 __global__ void pack_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
                             int64_t Lp, int D, int DP, double coord_scale, int with_norm,
-                            int pair_interleaved, float *__restrict__ out) {
+                            float *__restrict__ out) {
   const int64_t total = n * Lp;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = t / Lp;
-    const int64_t p = t % Lp;
-    const int64_t pt = min(p, L - 1);  // repeat the last point (zero increments)
+    const int64_t pt = min(t % Lp, L - 1);  // repeat the last point (zero increments)
     const double *src = X + (s * L + pt) * d;
-    // row layout [t][DP]; pair-interleaved layout puts points 2h, 2h+1 side by
-    // side: [s][h][DP][2]
-    float *dst;
-    int stride;
-    if (pair_interleaved) {
-      dst = out + (s * Lp + (p & ~(int64_t)1)) * DP + (p & 1);
-      stride = 2;
-    } else {
-      dst = out + t * DP;
-      stride = 1;
-    }
+    float *dst = out + t * DP;
     double nrm = 0.0;
     for (int k = 0; k < D; ++k) {
       const float v = (k < d) ? (float)(src[k] * coord_scale) : 0.f;
-      dst[k * stride] = v;
+      dst[k] = v;
       nrm += (double)v * (double)v;  // n-term from the rounded coordinates
     }
-    dst[D * stride] = with_norm ? (float)(-0.5 * nrm) : 0.f;
-    for (int k = D + 1; k < DP; ++k) dst[k * stride] = 0.f;
+    dst[D] = with_norm ? (float)(-0.5 * nrm) : 0.f;
+    for (int k = D + 1; k < DP; ++k) dst[k] = 0.f;
   }
 }
 
@@ -66,7 +55,7 @@ Plan plan_for(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   pl.DP = pl.D + 4;
   pl.sw = next_pow2((int)((ly + C - 1) / C));
   if (lx < pl.sw) return pl;
-  if (((size_t)NSLOT * lx + 1) * pl.DP * sizeof(float) > SMEM_LIMIT) return pl;
+  if ((size_t)NSLOT * lx * pl.DP * sizeof(float) > SMEM_LIMIT) return pl;
   pl.segs = NWARPS * (32 / pl.sw);
   pl.linear = kind == SK_LINEAR;
   pl.ok = true;
@@ -82,19 +71,18 @@ double coord_scale(const sk_kernel_config &c) {
 }
 
 int pack(const double *X, int64_t n, int64_t L, int64_t d, int64_t Lp, const Plan &pl,
-         const sk_kernel_config &c, float *out, cudaStream_t st, int pair_interleaved) {
+         const sk_kernel_config &c, float *out, cudaStream_t st) {
   const int64_t total = n * Lp;
   if (total <= 0) return SK_OK;
   const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 16);
   pack_kernel<<<(unsigned)blocks, 256, 0, st>>>(X, n, L, d, Lp, pl.D, pl.DP, coord_scale(c),
-                                                 pl.linear ? 0 : 1, pair_interleaved, out);
+                                                 pl.linear ? 0 : 1, out);
   SK_CHECK_LAUNCH();
   return SK_OK;
 }
 
 int launch(const Params &P, const Plan &pl, int M, cudaStream_t st) {
-  // + one pad row: the register prefetch reads one row past the last slot
-  const size_t smem = ((size_t)NSLOT * P.lx + 1) * pl.DP * sizeof(float);
+  const size_t smem = (size_t)NSLOT * P.lx * pl.DP * sizeof(float);
   switch (pl.D) {
     case 4:
       return launch_d4(P, M, pl.linear, smem, st);
@@ -117,18 +105,18 @@ bool fast_supported(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c
 size_t fast_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int64_t d,
                             const sk_kernel_config &c) {
   using namespace fast;
-  // x role: row layout [n][l][DP]; y role: pair-interleaved [n][sw*C][DP]
-  auto two_roles = [](int64_t na, int64_t la, int64_t nb, const Plan &pl) {
-    return align256((size_t)na * la * pl.DP * 4) + align256((size_t)nb * pl.sw * C * pl.DP * 4);
-  };
   size_t need = 0;
   const Plan px = plan_for(lx, lx, d, c);
-  if (px.ok) need = std::max(need, two_roles(nx, lx, nx, px));  // self levels of X / K(X)
+  if (px.ok)  // self levels of X (also the symmetric Gram)
+    need = std::max(need, align256((size_t)nx * std::max<int64_t>(lx, px.sw * C) * px.DP * 4));
   if (ny > 0) {
     const Plan py = plan_for(ly, ly, d, c);
-    if (py.ok) need = std::max(need, two_roles(ny, ly, ny, py));
+    if (py.ok)
+      need = std::max(need, align256((size_t)ny * std::max<int64_t>(ly, py.sw * C) * py.DP * 4));
     const Plan pg = plan_for(lx, ly, d, c);
-    if (pg.ok) need = std::max(need, two_roles(nx, lx, ny, pg));
+    if (pg.ok)
+      need = std::max(need, align256((size_t)nx * lx * pg.DP * 4) +
+                                align256((size_t)ny * pg.sw * C * pg.DP * 4));
   }
   return need;
 }
@@ -147,18 +135,27 @@ int fast_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t 
   const Plan pl = plan_for(lx, ly, d, c);
   if (!pl.ok) return fail(SK_ERR_UNSUPPORTED, "fast path does not cover this configuration");
   Params P{};
-  {
+  float *wsf = (float *)ws;
+  if (symmetric) {
+    const int64_t Lp = std::max<int64_t>(lx, pl.sw * C);
+    const size_t need = align256((size_t)nx * Lp * pl.DP * 4);
+    if (!ws || ws_bytes < need)
+      return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
+    int rc = pack(X, nx, lx, d, Lp, pl, c, wsf, st);
+    if (rc) return rc;
+    P.xs = P.ys = wsf;
+    P.lxp = P.lyp = (int)Lp;
+  } else {
     const size_t bx = align256((size_t)nx * lx * pl.DP * 4);
     const size_t by = align256((size_t)ny * pl.sw * C * pl.DP * 4);
     if (!ws || ws_bytes < bx + by)
       return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(bx + by));
-    float *xsb = (float *)ws;
     float *ysb = (float *)((char *)ws + bx);
-    int rc = pack(X, nx, lx, d, lx, pl, c, xsb, st, 0);
+    int rc = pack(X, nx, lx, d, lx, pl, c, wsf, st);
     if (rc) return rc;
-    rc = pack(Y, ny, ly, d, (int64_t)pl.sw * C, pl, c, ysb, st, 1);
+    rc = pack(Y, ny, ly, d, (int64_t)pl.sw * C, pl, c, ysb, st);
     if (rc) return rc;
-    P.xs = xsb;
+    P.xs = wsf;
     P.ys = ysb;
     P.lxp = (int)lx;
     P.lyp = pl.sw * C;
@@ -194,21 +191,16 @@ int fast_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
   const Plan pl = plan_for(l, l, d, c);
   if (!pl.ok) return fail(SK_ERR_UNSUPPORTED, "fast path does not cover this configuration");
   if (n <= 0) return SK_OK;
-  const size_t bx = align256((size_t)n * l * pl.DP * 4);
-  const size_t by = align256((size_t)n * pl.sw * C * pl.DP * 4);
-  if (!ws || ws_bytes < bx + by)
-    return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(bx + by));
-  float *xsb = (float *)ws;
-  float *ysb = (float *)((char *)ws + bx);
-  int rc = pack(X, n, l, d, l, pl, c, xsb, st, 0);
-  if (rc) return rc;
-  rc = pack(X, n, l, d, (int64_t)pl.sw * C, pl, c, ysb, st, 1);
+  const int64_t Lp = std::max<int64_t>(l, pl.sw * C);
+  const size_t need = align256((size_t)n * Lp * pl.DP * 4);
+  if (!ws || ws_bytes < need)
+    return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
+  float *wsf = (float *)ws;
+  int rc = pack(X, n, l, d, Lp, pl, c, wsf, st);
   if (rc) return rc;
   Params P{};
-  P.xs = xsb;
-  P.ys = ysb;
-  P.lxp = (int)l;
-  P.lyp = pl.sw * C;
+  P.xs = P.ys = wsf;
+  P.lxp = P.lyp = (int)Lp;
   P.nx = P.ny = n;
   P.lx = (int)l;
   P.sw = pl.sw;

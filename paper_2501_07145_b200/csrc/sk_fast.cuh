@@ -131,114 +131,33 @@ __device__ __forceinline__ void write_pair(const Params &P, int64_t i, int64_t j
   }
 }
 
-// Packed FP32 pairs (sm_100a FFMA2/FADD2): two adjacent columns of a lane
-// share one 64-bit register pair, halving issue slots for the FMA-pipe work.
-// Each half is an ordinary IEEE fp32 op, so results equal the scalar code.
-typedef unsigned long long f32x2;
-
-__device__ __forceinline__ f32x2 pk2(float lo, float hi) {
-  f32x2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ float lo2(f32x2 v) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-  return a;
-}
-__device__ __forceinline__ float hi2(f32x2 v) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-  return b;
-}
-__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
-  f32x2 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b) {
-  f32x2 d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f32x2 fsub2(f32x2 a, f32x2 b) {
-  f32x2 d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-
 // Per-lane register state of one segment lane and the systolic step.
 template <int D, int M, bool LINEAR>
 struct LaneState {
   static constexpr int DP = D + 4;
   static constexpr int NCA = (M >= 2) ? M - 1 : 0;  // column-accumulated levels 1..M-1
   static constexpr int NCR = (NCA > 0) ? NCA : 1;
-  static constexpr int H = C / 2;                    // column pairs per lane
 
-  f32x2 yv[H][D];       // (y[2h][k], y[2h+1][k])
-  f32x2 yn[H];          // n-terms of the column pair
-  f32x2 colacc[NCR][H];
-  f32x2 prevG[H];
-  f32x2 kM;             // level-M partial sums (two halves)
+  float yv[C][D];
+  float yn[C];
+  float colacc[NCR][C];
+  float prevG[C];
   float cout[NCR];
-  float kout, lastD;
-
-  struct Row {
-    float4 v[D / 4];
-    float n;
-  };
-
-  __device__ __forceinline__ static void load_row(Row &r, const float *__restrict__ p) {
-    const float4 *p4 = reinterpret_cast<const float4 *>(p);
-#pragma unroll
-    for (int k4 = 0; k4 < D / 4; ++k4) r.v[k4] = p4[k4];
-    r.n = LINEAR ? 0.f : p[D];
-  }
-
-  // yp: this lane's C columns in the pair-interleaved y layout: per column
-  // pair h, DP float2 entries (y[2h][k], y[2h+1][k]) for k < D, then the
-  // n-terms (n[2h], n[2h+1]). 16-byte loads land directly in aligned
-  // register pairs, which is what FFMA2 needs.
-  __device__ __forceinline__ void load_columns(const float *__restrict__ yp) {
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-      const float4 *p4 = reinterpret_cast<const float4 *>(yp + h * 2 * DP);
-#pragma unroll
-      for (int k2 = 0; k2 < D / 2; ++k2) {
-        const float4 u = __ldg(p4 + k2);
-        yv[h][2 * k2 + 0] = pk2(u.x, u.y);
-        yv[h][2 * k2 + 1] = pk2(u.z, u.w);
-      }
-      const float4 n = __ldg(p4 + D / 2);
-      yn[h] = LINEAR ? pk2(0.f, 0.f) : pk2(n.x, n.y);
-      prevG[h] = pk2(0.f, 0.f);
-    }
-  }
+  float kM, kout, lastD;
 
   __device__ __forceinline__ void reset_pair() {
 #pragma unroll
-    for (int h = 0; h < H; ++h) {
+    for (int c = 0; c < C; ++c) {
 #pragma unroll
-      for (int m = 0; m < NCR; ++m) colacc[m][h] = 0ull;
+      for (int m = 0; m < NCR; ++m) colacc[m][c] = 0.f;
     }
-    kM = 0ull;
-  }
-
-  // Zero the accumulators if this lane is at its pair boundary (predicated,
-  // no divergent branch).
-  __device__ __forceinline__ void reset_if(bool at_boundary) {
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-#pragma unroll
-      for (int m = 0; m < NCR; ++m) colacc[m][h] = at_boundary ? 0ull : colacc[m][h];
-    }
-    kM = at_boundary ? 0ull : kM;
+    kM = 0.f;
   }
 
   // One row of this lane's C columns. KCHAIN: also run the level-M chain
   // (only needed while some lane of the segment is at a pair boundary).
   template <bool KCHAIN>
-  __device__ __forceinline__ void step(const Row &xrow, int sw, bool first_lane) {
+  __device__ __forceinline__ void step(const float *__restrict__ xptr, int sw, bool first_lane) {
     constexpr unsigned FULL = 0xffffffffu;
     // (a) chain values produced by lane q-1 on the previous step
     const float dl_raw = __shfl_up_sync(FULL, lastD, 1, sw);
@@ -250,85 +169,73 @@ struct LaneState {
     }
     if (KCHAIN) {
       const float kin = __shfl_up_sync(FULL, kout, 1, sw);
-      kout = (first_lane ? 0.f : kin) + (lo2(kM) + hi2(kM));  // complete at the boundary
+      kout = (first_lane ? 0.f : kin) + kM;  // complete at this lane's pair boundary
     }
 
-    // (b) point-kernel row for this lane's columns: D FFMA2 per column pair
-    f32x2 g[H];
+    // (b) point-kernel row for this lane's columns
+    float g[C];
     {
-      f32x2 acc[H];
+      float acc[C];
 #pragma unroll
-      for (int h = 0; h < H; ++h) acc[h] = yn[h];
+      for (int c = 0; c < C; ++c) acc[c] = yn[c];
+      const float4 *xr = reinterpret_cast<const float4 *>(xptr);
 #pragma unroll
       for (int k4 = 0; k4 < D / 4; ++k4) {
-        const float4 xv = xrow.v[k4];
-        const f32x2 bx = pk2(xv.x, xv.x), by = pk2(xv.y, xv.y);
-        const f32x2 bz = pk2(xv.z, xv.z), bw = pk2(xv.w, xv.w);
+        const float4 xv = xr[k4];
 #pragma unroll
-        for (int h = 0; h < H; ++h) {
-          acc[h] = ffma2(bx, yv[h][4 * k4 + 0], acc[h]);
-          acc[h] = ffma2(by, yv[h][4 * k4 + 1], acc[h]);
-          acc[h] = ffma2(bz, yv[h][4 * k4 + 2], acc[h]);
-          acc[h] = ffma2(bw, yv[h][4 * k4 + 3], acc[h]);
+        for (int c = 0; c < C; ++c) {
+          acc[c] = fmaf(xv.x, yv[c][4 * k4 + 0], acc[c]);
+          acc[c] = fmaf(xv.y, yv[c][4 * k4 + 1], acc[c]);
+          acc[c] = fmaf(xv.z, yv[c][4 * k4 + 2], acc[c]);
+          acc[c] = fmaf(xv.w, yv[c][4 * k4 + 3], acc[c]);
         }
       }
       if (LINEAR) {
 #pragma unroll
-        for (int h = 0; h < H; ++h) g[h] = acc[h];
+        for (int c = 0; c < C; ++c) g[c] = acc[c];
       } else {
-        const f32x2 bn = pk2(xrow.n, xrow.n);
+        const float xn = xptr[D];
 #pragma unroll
-        for (int h = 0; h < H; ++h) {
-          const f32x2 t = fadd2(acc[h], bn);
-          g[h] = pk2(ex2_approx(fminf(lo2(t), 0.f)), ex2_approx(fminf(hi2(t), 0.f)));
-        }
+        for (int c = 0; c < C; ++c) g[c] = ex2_approx(fminf(acc[c] + xn, 0.f));
       }
     }
 
     // (c) increments of the previous DP row: A = D(g) - D(g-1), D = G(r,.) - G(r-1,.)
-    f32x2 A[H];
+    float a[C];
     {
       float dv[C];
 #pragma unroll
-      for (int h = 0; h < H; ++h) {
-        const f32x2 dd = fsub2(g[h], prevG[h]);
-        prevG[h] = g[h];
-        dv[2 * h] = lo2(dd);
-        dv[2 * h + 1] = hi2(dd);
+      for (int c = 0; c < C; ++c) {
+        dv[c] = g[c] - prevG[c];
+        prevG[c] = g[c];
       }
       const float dl = first_lane ? dv[0] : dl_raw;  // column -1 does not exist: A = 0
-      float a[C];
       a[0] = dv[0] - dl;
 #pragma unroll
       for (int c = 1; c < C; ++c) a[c] = dv[c] - dv[c - 1];
       lastD = dv[C - 1];
-#pragma unroll
-      for (int h = 0; h < H; ++h) A[h] = pk2(a[2 * h], a[2 * h + 1]);
     }
 
-    // (d) level recursion along the row (p = 1): R_m = A * S(R_{m-1});
-    // serial scan per column, column-pair updates with FFMA2
+    // (d) level recursion along the row (p = 1): R_m = A * S(R_{m-1})
     if constexpr (M == 1) {
 #pragma unroll
-      for (int h = 0; h < H; ++h) kM = fadd2(kM, A[h]);
+      for (int c = 0; c < C; ++c) kM += a[c];
     } else {
       float sc[NCR];
 #pragma unroll
       for (int m = 0; m < NCA; ++m) sc[m] = cin[m];
 #pragma unroll
-      for (int h = 0; h < H; ++h) {
-        float s0[NCR], s1[NCR];
+      for (int c = 0; c < C; ++c) {
+        float so[NCR];
 #pragma unroll
         for (int m = 0; m < NCA; ++m) {
-          s0[m] = sc[m];
-          s1[m] = s0[m] + lo2(colacc[m][h]);
-          sc[m] = s1[m] + hi2(colacc[m][h]);
+          so[m] = sc[m];
+          sc[m] += colacc[m][c];
         }
-        colacc[0][h] = fadd2(colacc[0][h], A[h]);
+        colacc[0][c] += a[c];
 #pragma unroll
-        for (int m = 1; m < NCA; ++m)
-          colacc[m][h] = ffma2(A[h], pk2(s0[m - 1], s1[m - 1]), colacc[m][h]);
-        kM = ffma2(A[h], pk2(s0[NCA - 1], s1[NCA - 1]), kM);
+        for (int m = 1; m < NCA; ++m) colacc[m][c] = fmaf(a[c], so[m - 1], colacc[m][c]);
+        kM = fmaf(a[c], so[NCA - 1], kM);
       }
 #pragma unroll
       for (int m = 0; m < NCA; ++m) cout[m] = sc[m];
@@ -373,7 +280,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) gram_p1_kernel(const Params P) {
     const int64_t jj = jvalid ? j : P.ny - 1;
 
     // this lane's y columns (pre-scaled points and their n-terms)
-    st.load_columns(P.ys + ((size_t)jj * P.lyp + (size_t)q * C) * DP);
+    {
+      const float *yp = P.ys + ((size_t)jj * P.lyp + (size_t)q * C) * DP;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+#pragma unroll
+        for (int k4 = 0; k4 < D / 4; ++k4) {
+          const float4 v = __ldg(reinterpret_cast<const float4 *>(yp + c * DP) + k4);
+          st.yv[c][4 * k4 + 0] = v.x;
+          st.yv[c][4 * k4 + 1] = v.y;
+          st.yv[c][4 * k4 + 2] = v.z;
+          st.yv[c][4 * k4 + 3] = v.w;
+        }
+        st.yn[c] = LINEAR ? 0.f : __ldg(yp + c * DP + D);
+        st.prevG[c] = 0.f;
+      }
+    }
     st.reset_pair();
     st.kout = st.lastD = 0.f;
 #pragma unroll
@@ -396,30 +318,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) gram_p1_kernel(const Params P) {
       const float *prev = (e == 0) ? smem : smem + ((e + NSLOT - 1) % NSLOT) * slot_floats;
       const int steps = (e < njobs) ? lx : sw;
       const int nA = min(sw, steps);
-      // x row of step s for this lane (row prefetched one step ahead)
-      auto row_ptr = [&](int s) {
-        return (s < q) ? prev + (lx - q + s) * DP : cur + (s - q) * DP;
-      };
-      typename LS::Row xa;
-      LS::load_row(xa, row_ptr(0));
       for (int s = 0; s < nA; ++s) {
-        typename LS::Row xb;
-        LS::load_row(xb, row_ptr(s + 1));  // may touch the pad row past the ring
-        st.template step<true>(xa, sw, first_lane);
-        // pair boundary of lane q is step s == q: pair e-1 is complete there
-        if (s == sw - 1 && e >= 1) {  // warp-uniform: the segments' last lanes finish
-          if (last_lane && jvalid) write_pair<M>(P, x0 + e - 1, j, st.cout, st.kout);
+        const float *xp = (s < q) ? prev + (lx - q + s) * DP : cur + (s - q) * DP;
+        st.template step<true>(xp, sw, first_lane);
+        if (s == q) {  // this lane's pair boundary: pair e-1 is complete
+          if (last_lane && e >= 1 && jvalid) write_pair<M>(P, x0 + e - 1, j, st.cout, st.kout);
+          st.reset_pair();
         }
-        st.reset_if(s == q);
-        xa = xb;
       }
-      const float *xp = cur + (nA - q + 1) * DP;
+      const float *xp = cur + (nA - q) * DP;
 #pragma unroll 2
       for (int s = nA; s < steps; ++s) {
-        typename LS::Row xb;
-        LS::load_row(xb, xp);
-        st.template step<false>(xa, sw, first_lane);
-        xa = xb;
+        st.template step<false>(xp, sw, first_lane);
         xp += DP;
       }
     }
@@ -431,7 +341,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gram_p1_kernel(const Params P) {
 // repeating the last point.
 __global__ void pack_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
                             int64_t Lp, int D, int DP, double coord_scale, int with_norm,
-                            int pair_interleaved, float *__restrict__ out);
+                            float *__restrict__ out);
 
 using LaunchFn = int (*)(const Params &, int M, int linear, size_t smem, cudaStream_t st);
 int launch_d4(const Params &, int M, int linear, size_t smem, cudaStream_t st);
