@@ -30,9 +30,11 @@ __global__ void pack_kernel(const double *__restrict__ X, int64_t n, int64_t L, 
 
 namespace {
 
+constexpr int RX_MULTI = 8;  // x sequences per tile when the carry buffer is in use
+
 struct Plan {
   bool ok = false;
-  int D = 0, DP = 0, sw = 0, segs = 0;
+  int D = 0, DP = 0, sw = 0, segs = 0, npanel = 1, nhp = 0;
   bool linear = false;
 };
 
@@ -50,12 +52,20 @@ Plan plan_for(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   if (c.precision != SK_PREC_FP32 || !c.difference) return pl;
   if (kind != SK_RBF && kind != SK_LINEAR) return pl;
   if (c.n_levels < 1 || c.n_levels > 8 || c.order != 1) return pl;
-  if (d < 1 || d > 16 || lx < 2 || ly < 2 || ly > 32 * C) return pl;
+  if (d < 1 || d > 16 || lx < 2 || ly < 2) return pl;
   pl.D = d <= 4 ? 4 : (d <= 8 ? 8 : 16);
   pl.DP = pl.D + 4;
-  pl.sw = next_pow2((int)((ly + C - 1) / C));
+  if (ly <= 32 * C) {
+    pl.sw = next_pow2((int)((ly + C - 1) / C));
+  } else {  // sequential 256-column panels with chain carries through HBM/L2
+    pl.sw = 32;
+    pl.npanel = (int)((ly + 32 * C - 1) / (32 * C));
+    const int nca = c.n_levels >= 2 ? c.n_levels - 1 : 0;
+    pl.nhp = (nca + 2 + 3) / 4 * 4;
+  }
   if (lx < pl.sw) return pl;
-  if ((size_t)NSLOT * lx * pl.DP * sizeof(float) > SMEM_LIMIT) return pl;
+  // + one pad row: the row prefetch may read one row past the last slot
+  if (((size_t)NSLOT * lx + 1) * pl.DP * sizeof(float) > SMEM_LIMIT) return pl;
   pl.segs = NWARPS * (32 / pl.sw);
   pl.linear = kind == SK_LINEAR;
   pl.ok = true;
@@ -63,6 +73,13 @@ Plan plan_for(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
 }
 
 size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+int lyp_of(const Plan &pl) { return pl.sw * C * pl.npanel; }
+
+size_t carry_bytes(int64_t lx, const Plan &pl) {
+  if (pl.npanel <= 1) return 0;
+  return align256((size_t)sm_count() * NWARPS * (RX_MULTI + 2) * lx * pl.nhp * sizeof(float));
+}
 
 double coord_scale(const sk_kernel_config &c) {
   if (c.static_spec.kind == SK_LINEAR) return std::sqrt(c.static_spec.scale);
@@ -82,7 +99,8 @@ int pack(const double *X, int64_t n, int64_t L, int64_t d, int64_t Lp, const Pla
 }
 
 int launch(const Params &P, const Plan &pl, int M, cudaStream_t st) {
-  const size_t smem = (size_t)NSLOT * P.lx * pl.DP * sizeof(float);
+  // + one pad row: the row prefetch may read one row past the last slot
+  const size_t smem = ((size_t)NSLOT * P.lx + 1) * pl.DP * sizeof(float);
   switch (pl.D) {
     case 4:
       return launch_d4(P, M, pl.linear, smem, st);
@@ -93,6 +111,67 @@ int launch(const Params &P, const Plan &pl, int M, cudaStream_t st) {
     default:
       return fail(SK_ERR_UNSUPPORTED, "fast path: unsupported channel padding");
   }
+}
+
+// Pack both roles into the workspace: x rows [rows][lxp], y columns [n][lyp]
+// (one shared array when x and y are the same sequences).
+struct Packed {
+  const float *xs, *ys;
+  int lxp, lyp;
+  float *carry;
+};
+
+int pack_roles(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
+               int64_t ly, int64_t d, bool same, const Plan &pl, const sk_kernel_config &c,
+               void *ws, size_t ws_bytes, cudaStream_t st, Packed &out) {
+  const int64_t lyp = lyp_of(pl);
+  size_t need;
+  if (same) {
+    const int64_t Lp = std::max<int64_t>(lx, lyp);
+    const size_t b = align256((size_t)nx * Lp * pl.DP * 4);
+    need = b + carry_bytes(lx, pl);
+    if (!ws || ws_bytes < need)
+      return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
+    int rc = pack(X, nx, lx, d, Lp, pl, c, (float *)ws, st);
+    if (rc) return rc;
+    out.xs = out.ys = (const float *)ws;
+    out.lxp = out.lyp = (int)Lp;
+    out.carry = (float *)((char *)ws + b);
+  } else {
+    const size_t bx = align256((size_t)nx * lx * pl.DP * 4);
+    const size_t by = align256((size_t)ny * lyp * pl.DP * 4);
+    need = bx + by + carry_bytes(lx, pl);
+    if (!ws || ws_bytes < need)
+      return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
+    float *xsb = (float *)ws;
+    float *ysb = (float *)((char *)ws + bx);
+    int rc = pack(X, nx, lx, d, lx, pl, c, xsb, st);
+    if (rc) return rc;
+    rc = pack(Y, ny, ly, d, lyp, pl, c, ysb, st);
+    if (rc) return rc;
+    out.xs = xsb;
+    out.ys = ysb;
+    out.lxp = (int)lx;
+    out.lyp = (int)lyp;
+    out.carry = (float *)((char *)ws + bx + by);
+  }
+  return SK_OK;
+}
+
+Params base_params(const Plan &pl, const Packed &pk, int64_t lx) {
+  Params P{};
+  P.xs = pk.xs;
+  P.ys = pk.ys;
+  P.lxp = pk.lxp;
+  P.lyp = pk.lyp;
+  P.lx = (int)lx;
+  P.sw = pl.sw;
+  P.segs = pl.segs;
+  P.npanel = pl.npanel;
+  P.nhp = pl.nhp;
+  P.carry = pk.carry;
+  P.max_ctas = sm_count();
+  return P;
 }
 
 }  // namespace
@@ -108,15 +187,17 @@ size_t fast_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int6
   size_t need = 0;
   const Plan px = plan_for(lx, lx, d, c);
   if (px.ok)  // self levels of X (also the symmetric Gram)
-    need = std::max(need, align256((size_t)nx * std::max<int64_t>(lx, px.sw * C) * px.DP * 4));
+    need = std::max(need, align256((size_t)nx * std::max<int64_t>(lx, lyp_of(px)) * px.DP * 4) +
+                              carry_bytes(lx, px));
   if (ny > 0) {
     const Plan py = plan_for(ly, ly, d, c);
     if (py.ok)
-      need = std::max(need, align256((size_t)ny * std::max<int64_t>(ly, py.sw * C) * py.DP * 4));
+      need = std::max(need, align256((size_t)ny * std::max<int64_t>(ly, lyp_of(py)) * py.DP * 4) +
+                                carry_bytes(ly, py));
     const Plan pg = plan_for(lx, ly, d, c);
     if (pg.ok)
       need = std::max(need, align256((size_t)nx * lx * pg.DP * 4) +
-                                align256((size_t)ny * pg.sw * C * pg.DP * 4));
+                                align256((size_t)ny * lyp_of(pg) * pg.DP * 4) + carry_bytes(lx, pg));
   }
   return need;
 }
@@ -134,42 +215,18 @@ int fast_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t 
   }
   const Plan pl = plan_for(lx, ly, d, c);
   if (!pl.ok) return fail(SK_ERR_UNSUPPORTED, "fast path does not cover this configuration");
-  Params P{};
-  float *wsf = (float *)ws;
-  if (symmetric) {
-    const int64_t Lp = std::max<int64_t>(lx, pl.sw * C);
-    const size_t need = align256((size_t)nx * Lp * pl.DP * 4);
-    if (!ws || ws_bytes < need)
-      return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
-    int rc = pack(X, nx, lx, d, Lp, pl, c, wsf, st);
-    if (rc) return rc;
-    P.xs = P.ys = wsf;
-    P.lxp = P.lyp = (int)Lp;
-  } else {
-    const size_t bx = align256((size_t)nx * lx * pl.DP * 4);
-    const size_t by = align256((size_t)ny * pl.sw * C * pl.DP * 4);
-    if (!ws || ws_bytes < bx + by)
-      return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(bx + by));
-    float *ysb = (float *)((char *)ws + bx);
-    int rc = pack(X, nx, lx, d, lx, pl, c, wsf, st);
-    if (rc) return rc;
-    rc = pack(Y, ny, ly, d, (int64_t)pl.sw * C, pl, c, ysb, st);
-    if (rc) return rc;
-    P.xs = wsf;
-    P.ys = ysb;
-    P.lxp = (int)lx;
-    P.lyp = pl.sw * C;
-  }
+  Packed pk{};
+  int rc = pack_roles(X, nx, lx, Y, ny, ly, d, symmetric != 0, pl, c, ws, ws_bytes, st, pk);
+  if (rc) return rc;
+  Params P = base_params(pl, pk, lx);
   P.nx = nx;
   P.ny = ny;
-  P.lx = (int)lx;
-  P.sw = pl.sw;
-  P.segs = pl.segs;
   P.tiles_y = (ny + pl.segs - 1) / pl.segs;
   const int64_t rows = row_end - row_begin;
   if (rows <= 0 || ny <= 0) return SK_OK;
   const int64_t target = (int64_t)sm_count() * 8;
-  P.rx = (int)std::max<int64_t>(1, std::min<int64_t>(64, (rows * P.tiles_y + target - 1) / target));
+  const int rx_cap = pl.npanel > 1 ? RX_MULTI : 64;
+  P.rx = (int)std::max<int64_t>(1, std::min<int64_t>(rx_cap, (rows * P.tiles_y + target - 1) / target));
   P.ntiles = ((rows + P.rx - 1) / P.rx) * P.tiles_y;
   P.row_begin = row_begin;
   P.row_end = row_end;
@@ -191,20 +248,13 @@ int fast_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
   const Plan pl = plan_for(l, l, d, c);
   if (!pl.ok) return fail(SK_ERR_UNSUPPORTED, "fast path does not cover this configuration");
   if (n <= 0) return SK_OK;
-  const int64_t Lp = std::max<int64_t>(l, pl.sw * C);
-  const size_t need = align256((size_t)n * Lp * pl.DP * 4);
-  if (!ws || ws_bytes < need)
-    return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
-  float *wsf = (float *)ws;
-  int rc = pack(X, n, l, d, Lp, pl, c, wsf, st);
+  Packed pk{};
+  int rc = pack_roles(X, n, l, X, n, l, d, true, pl, c, ws, ws_bytes, st, pk);
   if (rc) return rc;
-  Params P{};
-  P.xs = P.ys = wsf;
-  P.lxp = P.lyp = (int)Lp;
+  // each CTA evaluates its segments' y against the same sequences as x and
+  // keeps the diagonal: the same kernel and arithmetic as the Gram's diagonal
+  Params P = base_params(pl, pk, l);
   P.nx = P.ny = n;
-  P.lx = (int)l;
-  P.sw = pl.sw;
-  P.segs = pl.segs;
   P.tiles_y = (n + pl.segs - 1) / pl.segs;
   P.ntiles = P.tiles_y;
   P.rx = pl.segs;

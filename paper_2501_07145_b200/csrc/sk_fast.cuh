@@ -74,6 +74,12 @@ struct Params {
   int64_t ldk;
   double *levels;
   double *self_out;
+  // multi-panel (L_y > 256): the pair's columns are swept in npanel passes of
+  // 256 columns; chain values cross panel boundaries through `carry`
+  int npanel;
+  float *carry;  // [max_ctas * NWARPS][rx + 2 jobs][lx rows][nhp]
+  int nhp;       // floats per carry entry (NCA chain values, lastD, kout; padded to 4)
+  int max_ctas;  // grid size the carry buffer was sized for
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -156,20 +162,25 @@ struct LaneState {
 
   // One row of this lane's C columns. KCHAIN: also run the level-M chain
   // (only needed while some lane of the segment is at a pair boundary).
-  template <bool KCHAIN>
-  __device__ __forceinline__ void step(const float *__restrict__ xptr, int sw, bool first_lane) {
+  //  MULTI: the chain head takes its inputs from `hin` (the previous panel's
+  //         carries for this row) when head_buf, instead of zeros
+  template <bool KCHAIN, bool MULTI>
+  __device__ __forceinline__ void step(const float *__restrict__ xptr, int sw, bool first_lane,
+                                       const float *hin, bool head_buf) {
     constexpr unsigned FULL = 0xffffffffu;
+    const bool from_buf = MULTI && head_buf;
     // (a) chain values produced by lane q-1 on the previous step
-    const float dl_raw = __shfl_up_sync(FULL, lastD, 1, sw);
+    float dl_raw = __shfl_up_sync(FULL, lastD, 1, sw);
     float cin[NCR];
 #pragma unroll
     for (int m = 0; m < NCA; ++m) {
       const float v = __shfl_up_sync(FULL, cout[m], 1, sw);
-      cin[m] = first_lane ? 0.f : v;
+      cin[m] = first_lane ? (from_buf ? hin[m] : 0.f) : v;
     }
+    if (from_buf && first_lane) dl_raw = hin[NCA];
     if (KCHAIN) {
       const float kin = __shfl_up_sync(FULL, kout, 1, sw);
-      kout = (first_lane ? 0.f : kin) + kM;  // complete at this lane's pair boundary
+      kout = (first_lane ? (from_buf ? hin[NCA + 1] : 0.f) : kin) + kM;  // complete at a boundary
     }
 
     // (b) point-kernel row for this lane's columns
@@ -209,7 +220,9 @@ struct LaneState {
         dv[c] = g[c] - prevG[c];
         prevG[c] = g[c];
       }
-      const float dl = first_lane ? dv[0] : dl_raw;  // column -1 does not exist: A = 0
+      // column -1 of the first panel does not exist (A = 0); a later panel's
+      // head gets D of the previous panel's last column through the carry
+      const float dl = (first_lane && !from_buf) ? dv[0] : dl_raw;
       a[0] = dv[0] - dl;
 #pragma unroll
       for (int c = 1; c < C; ++c) a[c] = dv[c] - dv[c - 1];
@@ -243,7 +256,7 @@ struct LaneState {
   }
 };
 
-template <int D, int M, bool LINEAR>
+template <int D, int M, bool LINEAR, bool MULTI>
 __global__ void __launch_bounds__(NTHREADS, 1) gram_p1_kernel(const Params P) {
   static_assert(D % 4 == 0, "D must be a multiple of 4");
   static_assert(M >= 1, "M >= 1");
@@ -279,58 +292,109 @@ __global__ void __launch_bounds__(NTHREADS, 1) gram_p1_kernel(const Params P) {
     const bool jvalid = j < P.ny;
     const int64_t jj = jvalid ? j : P.ny - 1;
 
-    // this lane's y columns (pre-scaled points and their n-terms)
-    {
-      const float *yp = P.ys + ((size_t)jj * P.lyp + (size_t)q * C) * DP;
+    // carry region of this warp (multi-panel only)
+    float *cbuf = MULTI ? P.carry + ((size_t)(blockIdx.x * NWARPS + warp) * (P.rx + 2)) * lx * P.nhp
+                        : nullptr;
+    const int npanel = MULTI ? P.npanel : 1;
+    for (int pnl = 0; pnl < npanel; ++pnl) {
+      // this lane's y columns of panel pnl (pre-scaled points and their n-terms)
+      {
+        const float *yp = P.ys + ((size_t)jj * P.lyp + (size_t)pnl * 32 * C + (size_t)q * C) * DP;
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
+        for (int c = 0; c < C; ++c) {
 #pragma unroll
-        for (int k4 = 0; k4 < D / 4; ++k4) {
-          const float4 v = __ldg(reinterpret_cast<const float4 *>(yp + c * DP) + k4);
-          st.yv[c][4 * k4 + 0] = v.x;
-          st.yv[c][4 * k4 + 1] = v.y;
-          st.yv[c][4 * k4 + 2] = v.z;
-          st.yv[c][4 * k4 + 3] = v.w;
-        }
-        st.yn[c] = LINEAR ? 0.f : __ldg(yp + c * DP + D);
-        st.prevG[c] = 0.f;
-      }
-    }
-    st.reset_pair();
-    st.kout = st.lastD = 0.f;
-#pragma unroll
-    for (int m = 0; m < LS::NCR; ++m) st.cout[m] = 0.f;
-
-    __syncthreads();  // previous tile's readers are done with the ring
-    stage_sequence(smem, P.xs + (size_t)x0 * P.lxp * DP, slot_floats);
-
-    // Epoch e streams x_{x0+e}: lane q starts that pair at step s = q (its
-    // row 0) and spends steps s < q finishing pair e-1. So pair boundaries
-    // only occur in steps s < sw ("phase A"); steps s >= sw are branch-free.
-    for (int64_t e = 0; e <= njobs; ++e) {
-      cp_async_wait_all();
-      __syncthreads();
-      if (e + 1 < njobs)
-        stage_sequence(smem + ((e + 1) % NSLOT) * slot_floats,
-                       P.xs + (size_t)(x0 + e + 1) * P.lxp * DP, slot_floats);
-      const float *cur = smem + (e % NSLOT) * slot_floats;
-      // before its first pair a lane idles on rows of x_{x0} (slot 0)
-      const float *prev = (e == 0) ? smem : smem + ((e + NSLOT - 1) % NSLOT) * slot_floats;
-      const int steps = (e < njobs) ? lx : sw;
-      const int nA = min(sw, steps);
-      for (int s = 0; s < nA; ++s) {
-        const float *xp = (s < q) ? prev + (lx - q + s) * DP : cur + (s - q) * DP;
-        st.template step<true>(xp, sw, first_lane);
-        if (s == q) {  // this lane's pair boundary: pair e-1 is complete
-          if (last_lane && e >= 1 && jvalid) write_pair<M>(P, x0 + e - 1, j, st.cout, st.kout);
-          st.reset_pair();
+          for (int k4 = 0; k4 < D / 4; ++k4) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(yp + c * DP) + k4);
+            st.yv[c][4 * k4 + 0] = v.x;
+            st.yv[c][4 * k4 + 1] = v.y;
+            st.yv[c][4 * k4 + 2] = v.z;
+            st.yv[c][4 * k4 + 3] = v.w;
+          }
+          st.yn[c] = LINEAR ? 0.f : __ldg(yp + c * DP + D);
+          st.prevG[c] = 0.f;
         }
       }
-      const float *xp = cur + (nA - q) * DP;
+      st.reset_pair();
+      st.kout = st.lastD = 0.f;
+#pragma unroll
+      for (int m = 0; m < LS::NCR; ++m) st.cout[m] = 0.f;
+      const bool head_buf = MULTI && pnl > 0;          // chain inputs from the previous panel
+      const bool tail_buf = MULTI && pnl < npanel - 1;  // chain outputs for the next panel
+      const bool last_panel = pnl == npanel - 1;
+
+      __syncthreads();  // previous readers are done with the ring (and the carries are visible)
+      stage_sequence(smem, P.xs + (size_t)x0 * P.lxp * DP, slot_floats);
+
+      // head inputs, prefetched one step ahead (lane 0 reads job e, row s)
+      constexpr int NHM = LS::NCA + 2;
+      float hcur[NHM], hnext[NHM];
+#pragma unroll
+      for (int k = 0; k < NHM; ++k) hcur[k] = hnext[k] = 0.f;
+      auto load_head = [&](float (&h)[NHM], int64_t job, int row) {
+        if (head_buf && first_lane) {
+          const float *src = cbuf + ((size_t)job * lx + row) * P.nhp;
+#pragma unroll
+          for (int k = 0; k < NHM; ++k) h[k] = src[k];
+        }
+      };
+      auto store_tail = [&](int64_t job, int row) {
+        if (tail_buf && last_lane && job >= 0) {
+          float *dst = cbuf + ((size_t)job * lx + row) * P.nhp;
+#pragma unroll
+          for (int m = 0; m < LS::NCA; ++m) dst[m] = st.cout[m];
+          dst[LS::NCA] = st.lastD;
+          dst[LS::NCA + 1] = st.kout;
+        }
+      };
+      load_head(hcur, 0, 0);
+
+      // Epoch e streams x_{x0+e}: lane q starts that pair at step s = q (its
+      // row 0) and spends steps s < q finishing pair e-1. So pair boundaries
+      // only occur in steps s < sw ("phase A"); steps s >= sw are branch-free.
+      for (int64_t e = 0; e <= njobs; ++e) {
+        cp_async_wait_all();
+        __syncthreads();
+        if (e + 1 < njobs)
+          stage_sequence(smem + ((e + 1) % NSLOT) * slot_floats,
+                         P.xs + (size_t)(x0 + e + 1) * P.lxp * DP, slot_floats);
+        const float *cur = smem + (e % NSLOT) * slot_floats;
+        // before its first pair a lane idles on rows of x_{x0} (slot 0)
+        const float *prev = (e == 0) ? smem : smem + ((e + NSLOT - 1) % NSLOT) * slot_floats;
+        const int steps = (e < njobs) ? lx : sw;
+        const int nA = min(sw, steps);
+        for (int s = 0; s < nA; ++s) {
+          if (MULTI) load_head(hnext, s + 1 < steps ? e : e + 1, s + 1 < steps ? s + 1 : 0);
+          const float *xp = (s < q) ? prev + (lx - q + s) * DP : cur + (s - q) * DP;
+          st.template step<true, MULTI>(xp, sw, first_lane, hcur, head_buf);
+          if (MULTI) {
+            // the segment's last lane is at (job, row) = (e, s - q) or (e - 1, lx - q + s)
+            if (s >= q)
+              store_tail(e, s - q);
+            else
+              store_tail(e - 1, lx - q + s);
+          }
+          if (s == q) {  // this lane's pair boundary: pair e-1 is complete
+            if (last_panel && last_lane && e >= 1 && jvalid)
+              write_pair<M>(P, x0 + e - 1, j, st.cout, st.kout);
+            st.reset_pair();
+          }
+          if (MULTI) {
+#pragma unroll
+            for (int k = 0; k < NHM; ++k) hcur[k] = hnext[k];
+          }
+        }
+        const float *xp = cur + (nA - q) * DP;
 #pragma unroll 2
-      for (int s = nA; s < steps; ++s) {
-        st.template step<false>(xp, sw, first_lane);
-        xp += DP;
+        for (int s = nA; s < steps; ++s) {
+          if (MULTI) load_head(hnext, s + 1 < steps ? e : e + 1, s + 1 < steps ? s + 1 : 0);
+          st.template step<false, MULTI>(xp, sw, first_lane, hcur, head_buf);
+          if (MULTI) {
+            store_tail(e, s - q);
+#pragma unroll
+            for (int k = 0; k < NHM; ++k) hcur[k] = hnext[k];
+          }
+          xp += DP;
+        }
       }
     }
   }
@@ -343,7 +407,6 @@ __global__ void pack_kernel(const double *__restrict__ X, int64_t n, int64_t L, 
                             int64_t Lp, int D, int DP, double coord_scale, int with_norm,
                             float *__restrict__ out);
 
-using LaunchFn = int (*)(const Params &, int M, int linear, size_t smem, cudaStream_t st);
 int launch_d4(const Params &, int M, int linear, size_t smem, cudaStream_t st);
 int launch_d8(const Params &, int M, int linear, size_t smem, cudaStream_t st);
 int launch_d16(const Params &, int M, int linear, size_t smem, cudaStream_t st);
@@ -353,9 +416,12 @@ template <int D>
 int launch_impl(const Params &P, int M, int linear, size_t smem, cudaStream_t st) {
   using K = void (*)(const Params);
   K k = nullptr;
-#define SK_CASE(MM)                                                        \
-  case MM:                                                                 \
-    k = linear ? gram_p1_kernel<D, MM, true> : gram_p1_kernel<D, MM, false>; \
+#define SK_CASE(MM)                                                                       \
+  case MM:                                                                                \
+    if (P.npanel > 1)                                                                     \
+      k = linear ? gram_p1_kernel<D, MM, true, true> : gram_p1_kernel<D, MM, false, true>;  \
+    else                                                                                  \
+      k = linear ? gram_p1_kernel<D, MM, true, false> : gram_p1_kernel<D, MM, false, false>; \
     break;
   switch (M) {
     SK_CASE(1)
@@ -374,7 +440,8 @@ int launch_impl(const Params &P, int M, int linear, size_t smem, cudaStream_t st
   int per_sm = 0;
   SK_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NTHREADS, smem));
   if (per_sm < 1) per_sm = 1;
-  const int64_t cap = (int64_t)sm_count() * per_sm;
+  int64_t cap = (int64_t)sm_count() * per_sm;
+  if (P.npanel > 1) cap = std::min<int64_t>(cap, P.max_ctas);  // carry buffer is sized per CTA
   const int grid = (int)std::min<int64_t>(P.ntiles, cap);
   if (grid <= 0) return SK_OK;
   k<<<grid, NTHREADS, smem, st>>>(P);

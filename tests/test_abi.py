@@ -48,7 +48,9 @@ def test_fast_path_selection():
     assert lib.sk_fast_path(256, 256, 16, f64) == 0
     mat = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="matern32")))
     assert lib.sk_fast_path(64, 64, 4, mat) == 0
-    assert lib.sk_fast_path(300, 300, 4, c3) == 0           # more columns than one warp holds
+    assert lib.sk_fast_path(300, 300, 4, c3) == 1           # two 256-column panels
+    assert lib.sk_fast_path(2048, 2048, 4, _native.config_struct(KernelConfig(n_levels=8))) == 1  # c5
+    assert lib.sk_fast_path(1000, 1000, 16, c3) == 0        # x ring would exceed shared memory
     assert lib.sk_fast_path(2, 256, 4, c3) == 0             # x shorter than the wavefront
 
 

@@ -133,6 +133,31 @@ def test_ragged_lengths_and_short_sequences():
     assert np.array_equal(K, np.ones((3, 5)))
 
 
+@pytest.mark.parametrize("lx,ly", [(300, 300), (260, 600), (600, 270)])
+def test_multi_panel_lengths(lx, ly):
+    """L_y > 256: sequential 256-column panels chained through the carry buffer."""
+    X = gen_brownian(6, lx, 4, SeedStream(11)).data
+    Y = gen_brownian(5, ly, 4, SeedStream(12)).data
+    for norm, tol in (("none", TOL_RAW), ("levelwise", TOL_NORM)):
+        cfg = KernelConfig(n_levels=6, normalization=norm)
+        assert uses_fast_path(lx, ly, 4, cfg)
+        R = sig_kernel_gram(X, Y, cfg=cfg, precision="fp64")
+        assert _rel(sig_kernel_gram(X, Y, cfg=cfg), R) <= tol, (lx, ly, norm)
+
+
+def test_multi_panel_symmetric_and_blocks():
+    from paper_2501_07145_b200.kernels import gram_block
+    X = gen_brownian(21, 520, 3, SeedStream(13)).data
+    cfg = KernelConfig(n_levels=4, normalization="levelwise")
+    K = sig_kernel_gram(X, cfg=cfg)
+    assert np.array_equal(K, K.T) and np.array_equal(np.diag(K), np.ones(21))
+    Xt = torch.from_numpy(X).cuda()
+    Y = torch.from_numpy(gen_brownian(9, 520, 3, SeedStream(14)).data).cuda()
+    full, _ = gram_block(Xt, Y, cfg)
+    parts = [gram_block(Xt, Y, cfg, r0, r1)[0] for r0, r1 in ((0, 5), (5, 21))]
+    assert torch.equal(torch.cat(parts), full)
+
+
 def test_levels_dp_golden(levels_golden):
     z = levels_golden
     for t in range(24):
