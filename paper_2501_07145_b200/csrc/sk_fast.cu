@@ -7,24 +7,57 @@
 namespace sk {
 namespace fast {
 
-__global__ void pack_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
-                            int64_t Lp, int D, int DP, double coord_scale, int with_norm,
-                            float *__restrict__ out) {
+// coordinate k of packed point r (rows beyond L repeat the last point);
+// incr: the increment x_r - x_{r-1} instead (0 for r = 0 and beyond L)
+__device__ __forceinline__ double packed_coord(const double *__restrict__ seq, int64_t L,
+                                               int64_t d, int64_t r, int k, int incr) {
+  const int64_t pt = min(r, L - 1);
+  double v = seq[pt * d + k];
+  if (incr) v = (r >= 1 && r < L) ? v - seq[(pt - 1) * d + k] : 0.0;
+  return v;
+}
+
+__global__ void pack_y_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
+                              int64_t Lp, int D, double coord_scale, int incr,
+                              float *__restrict__ out) {
+  const int YP = y_stride(D);
   const int64_t total = n * Lp;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = t / Lp;
-    const int64_t pt = min(t % Lp, L - 1);  // repeat the last point (zero increments)
-    const double *src = X + (s * L + pt) * d;
-    float *dst = out + t * DP;
+    const double *seq = X + s * L * d;
+    float *dst = out + t * YP;
     double nrm = 0.0;
     for (int k = 0; k < D; ++k) {
-      const float v = (k < d) ? (float)(src[k] * coord_scale) : 0.f;
+      const float v = (k < d) ? (float)(packed_coord(seq, L, d, t % Lp, k, incr) * coord_scale) : 0.f;
       dst[k] = v;
       nrm += (double)v * (double)v;  // n-term from the rounded coordinates
     }
-    dst[D] = with_norm ? (float)(-0.5 * nrm) : 0.f;
-    for (int k = D + 1; k < DP; ++k) dst[k] = 0.f;
+    dst[D] = incr ? 0.f : (float)(-0.5 * nrm);
+    for (int k = D + 1; k < YP; ++k) dst[k] = 0.f;
+  }
+}
+
+__global__ void pack_x_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
+                              int64_t Lp2, int D, double coord_scale, int incr,
+                              float *__restrict__ out) {
+  const int XP = x_stride(D);
+  const int64_t total = n * Lp2 * 2;  // one thread per (sequence, row)
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = t / (2 * Lp2);
+    const int64_t r = t % (2 * Lp2);
+    const int half = (int)(r & 1);
+    const double *seq = X + s * L * d;
+    float *dst = out + (s * Lp2 + (r >> 1)) * XP;
+    double nrm = 0.0;
+    for (int k = 0; k < D; ++k) {
+      const float v = (k < d) ? (float)(packed_coord(seq, L, d, r, k, incr) * coord_scale) : 0.f;
+      dst[2 * k + half] = v;
+      nrm += (double)v * (double)v;
+    }
+    dst[2 * D + half] = incr ? 0.f : (float)(-0.5 * nrm);
+    dst[2 * D + 2 + half] = 0.f;
   }
 }
 
@@ -34,7 +67,7 @@ constexpr int RX_MULTI = 8;  // x sequences per tile when the carry buffer is in
 
 struct Plan {
   bool ok = false;
-  int D = 0, DP = 0, sw = 0, segs = 0, npanel = 1, nhp = 0;
+  int D = 0, C = 8, sw = 0, segs = 0, npanel = 1, nhp = 0;
   bool linear = false;
 };
 
@@ -46,26 +79,36 @@ int next_pow2(int v) {
 
 constexpr size_t SMEM_LIMIT = 200 * 1024;
 
+int64_t pairs_of(int64_t lx) { return (lx + 1) / 2; }
+
 Plan plan_for(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   Plan pl;
   const int kind = c.static_spec.kind;
   if (c.precision != SK_PREC_FP32 || !c.difference) return pl;
   if (kind != SK_RBF && kind != SK_LINEAR) return pl;
-  if (c.n_levels < 1 || c.n_levels > 8 || c.order != 1) return pl;
+  if (!fast_orders_supported(c.n_levels, c.order)) return pl;
+  // Normalised linear kernels of order > 1 are sensitive to the FP32
+  // accumulation of the increment inner products (measured 1.6-2.1e-5 vs the
+  // 1e-5 bar, also in a float64-recursion emulation): float64 kernel.
+  if (kind == SK_LINEAR && c.order > 1 && c.normalization != SK_NORM_NONE) return pl;
   if (d < 1 || d > 16 || lx < 2 || ly < 2) return pl;
   pl.D = d <= 4 ? 4 : (d <= 8 ? 8 : 16);
-  pl.DP = pl.D + 4;
+  const int C = pl.C = columns_per_lane(c.order);
   if (ly <= 32 * C) {
     pl.sw = next_pow2((int)((ly + C - 1) / C));
-  } else {  // sequential 256-column panels with chain carries through HBM/L2
+  } else {  // sequential 32*C-column panels with chain carries through HBM/L2
     pl.sw = 32;
     pl.npanel = (int)((ly + 32 * C - 1) / (32 * C));
-    const int nca = c.n_levels >= 2 ? c.n_levels - 1 : 0;
-    pl.nhp = (nca + 2 + 3) / 4 * 4;
+    // chain values per row: p = 1: levels 1..M-1; general p: S and E chains
+    int nch = c.n_levels >= 2 ? c.n_levels - 1 : 0;
+    if (c.order > 1)
+      for (int m = 1; m < c.n_levels; ++m) nch += std::min(m + 1, (int)c.order) - 1;
+    pl.nhp = (2 * nch + 3 + 3) / 4 * 4;
   }
-  if (lx < pl.sw) return pl;
-  // + one pad row: the row prefetch may read one row past the last slot
-  if (((size_t)NSLOT * lx + 1) * pl.DP * sizeof(float) > SMEM_LIMIT) return pl;
+  const int64_t lx2 = pairs_of(lx);
+  if (lx2 < pl.sw) return pl;
+  // + one pad record: the row prefetch may read one record past the last slot
+  if (((size_t)NSLOT * lx2 + 1) * x_stride(pl.D) * sizeof(float) > SMEM_LIMIT) return pl;
   pl.segs = NWARPS * (32 / pl.sw);
   pl.linear = kind == SK_LINEAR;
   pl.ok = true;
@@ -74,11 +117,22 @@ Plan plan_for(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
 
 size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
-int lyp_of(const Plan &pl) { return pl.sw * C * pl.npanel; }
+int lyp_of(const Plan &pl) { return pl.sw * pl.C * pl.npanel; }
 
 size_t carry_bytes(int64_t lx, const Plan &pl) {
   if (pl.npanel <= 1) return 0;
-  return align256((size_t)sm_count() * NWARPS * (RX_MULTI + 2) * lx * pl.nhp * sizeof(float));
+  return align256((size_t)sm_count() * NWARPS * (RX_MULTI + 2) * pairs_of(lx) * pl.nhp *
+                  sizeof(float));
+}
+
+size_t x_bytes(int64_t n, int64_t lx, const Plan &pl) {
+  return align256((size_t)n * pairs_of(lx) * x_stride(pl.D) * sizeof(float));
+}
+size_t y_bytes(int64_t n, const Plan &pl) {
+  return align256((size_t)n * lyp_of(pl) * y_stride(pl.D) * sizeof(float));
+}
+size_t roles_bytes(int64_t nx, int64_t lx, int64_t ny, const Plan &pl) {
+  return x_bytes(nx, lx, pl) + y_bytes(ny, pl) + carry_bytes(lx, pl);
 }
 
 double coord_scale(const sk_kernel_config &c) {
@@ -87,84 +141,69 @@ double coord_scale(const sk_kernel_config &c) {
   return std::sqrt(1.4426950408889634) / c.static_spec.bandwidth;
 }
 
-int pack(const double *X, int64_t n, int64_t L, int64_t d, int64_t Lp, const Plan &pl,
-         const sk_kernel_config &c, float *out, cudaStream_t st) {
-  const int64_t total = n * Lp;
-  if (total <= 0) return SK_OK;
-  const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 16);
-  pack_kernel<<<(unsigned)blocks, 256, 0, st>>>(X, n, L, d, Lp, pl.D, pl.DP, coord_scale(c),
-                                                 pl.linear ? 0 : 1, out);
-  SK_CHECK_LAUNCH();
-  return SK_OK;
+unsigned pack_blocks(int64_t total) {
+  return (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 16);
 }
 
-int launch(const Params &P, const Plan &pl, int M, cudaStream_t st) {
-  // + one pad row: the row prefetch may read one row past the last slot
-  const size_t smem = ((size_t)NSLOT * P.lx + 1) * pl.DP * sizeof(float);
+int launch(const Params &P, const Plan &pl, int M, int order, cudaStream_t st) {
+  // + one pad record: the row prefetch may read one record past the last slot
+  const size_t smem = ((size_t)NSLOT * P.lx2 + 1) * x_stride(pl.D) * sizeof(float);
   switch (pl.D) {
     case 4:
-      return launch_d4(P, M, pl.linear, smem, st);
+      return launch_d4(P, M, order, pl.linear, smem, st);
     case 8:
-      return launch_d8(P, M, pl.linear, smem, st);
+      return launch_d8(P, M, order, pl.linear, smem, st);
     case 16:
-      return launch_d16(P, M, pl.linear, smem, st);
+      return launch_d16(P, M, order, pl.linear, smem, st);
     default:
       return fail(SK_ERR_UNSUPPORTED, "fast path: unsupported channel padding");
   }
 }
 
-// Pack both roles into the workspace: x rows [rows][lxp], y columns [n][lyp]
-// (one shared array when x and y are the same sequences).
+// Pack both roles into the workspace: x row pairs [nx][lx2], y columns
+// [ny][lyp], then the carry buffer.
 struct Packed {
   const float *xs, *ys;
-  int lxp, lyp;
+  int lx2, lyp;
   float *carry;
 };
 
 int pack_roles(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
-               int64_t ly, int64_t d, bool same, const Plan &pl, const sk_kernel_config &c,
-               void *ws, size_t ws_bytes, cudaStream_t st, Packed &out) {
-  const int64_t lyp = lyp_of(pl);
-  size_t need;
-  if (same) {
-    const int64_t Lp = std::max<int64_t>(lx, lyp);
-    const size_t b = align256((size_t)nx * Lp * pl.DP * 4);
-    need = b + carry_bytes(lx, pl);
-    if (!ws || ws_bytes < need)
-      return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
-    int rc = pack(X, nx, lx, d, Lp, pl, c, (float *)ws, st);
-    if (rc) return rc;
-    out.xs = out.ys = (const float *)ws;
-    out.lxp = out.lyp = (int)Lp;
-    out.carry = (float *)((char *)ws + b);
-  } else {
-    const size_t bx = align256((size_t)nx * lx * pl.DP * 4);
-    const size_t by = align256((size_t)ny * lyp * pl.DP * 4);
-    need = bx + by + carry_bytes(lx, pl);
-    if (!ws || ws_bytes < need)
-      return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
-    float *xsb = (float *)ws;
-    float *ysb = (float *)((char *)ws + bx);
-    int rc = pack(X, nx, lx, d, lx, pl, c, xsb, st);
-    if (rc) return rc;
-    rc = pack(Y, ny, ly, d, lyp, pl, c, ysb, st);
-    if (rc) return rc;
-    out.xs = xsb;
-    out.ys = ysb;
-    out.lxp = (int)lx;
-    out.lyp = (int)lyp;
-    out.carry = (float *)((char *)ws + bx + by);
+               int64_t ly, int64_t d, const Plan &pl, const sk_kernel_config &c, void *ws,
+               size_t ws_bytes, cudaStream_t st, Packed &out) {
+  const size_t need = roles_bytes(nx, lx, ny, pl);
+  if (!ws || ws_bytes < need)
+    return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
+  const size_t bx = x_bytes(nx, lx, pl), by = y_bytes(ny, pl);
+  float *xsb = (float *)ws;
+  float *ysb = (float *)((char *)ws + bx);
+  const int64_t lx2 = pairs_of(lx), lyp = lyp_of(pl);
+  const double cs = coord_scale(c);
+  const int incr = pl.linear ? 1 : 0;  // linear: A = <dx, dy> directly
+  if (nx > 0) {
+    pack_x_kernel<<<pack_blocks(nx * lx2 * 2), 256, 0, st>>>(X, nx, lx, d, lx2, pl.D, cs, incr,
+                                                             xsb);
+    SK_CHECK_LAUNCH();
   }
+  if (ny > 0) {
+    pack_y_kernel<<<pack_blocks(ny * lyp), 256, 0, st>>>(Y, ny, ly, d, lyp, pl.D, cs, incr,
+                                                         ysb);
+    SK_CHECK_LAUNCH();
+  }
+  out.xs = xsb;
+  out.ys = ysb;
+  out.lx2 = (int)lx2;
+  out.lyp = (int)lyp;
+  out.carry = (float *)((char *)ws + bx + by);
   return SK_OK;
 }
 
-Params base_params(const Plan &pl, const Packed &pk, int64_t lx) {
+Params base_params(const Plan &pl, const Packed &pk) {
   Params P{};
   P.xs = pk.xs;
   P.ys = pk.ys;
-  P.lxp = pk.lxp;
+  P.lx2 = pk.lx2;
   P.lyp = pk.lyp;
-  P.lx = (int)lx;
   P.sw = pl.sw;
   P.segs = pl.segs;
   P.npanel = pl.npanel;
@@ -186,18 +225,12 @@ size_t fast_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int6
   using namespace fast;
   size_t need = 0;
   const Plan px = plan_for(lx, lx, d, c);
-  if (px.ok)  // self levels of X (also the symmetric Gram)
-    need = std::max(need, align256((size_t)nx * std::max<int64_t>(lx, lyp_of(px)) * px.DP * 4) +
-                              carry_bytes(lx, px));
+  if (px.ok) need = std::max(need, roles_bytes(nx, lx, nx, px));  // self levels / K(X)
   if (ny > 0) {
     const Plan py = plan_for(ly, ly, d, c);
-    if (py.ok)
-      need = std::max(need, align256((size_t)ny * std::max<int64_t>(ly, lyp_of(py)) * py.DP * 4) +
-                                carry_bytes(ly, py));
+    if (py.ok) need = std::max(need, roles_bytes(ny, ly, ny, py));
     const Plan pg = plan_for(lx, ly, d, c);
-    if (pg.ok)
-      need = std::max(need, align256((size_t)nx * lx * pg.DP * 4) +
-                                align256((size_t)ny * lyp_of(pg) * pg.DP * 4) + carry_bytes(lx, pg));
+    if (pg.ok) need = std::max(need, roles_bytes(nx, lx, ny, pg));
   }
   return need;
 }
@@ -216,9 +249,9 @@ int fast_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t 
   const Plan pl = plan_for(lx, ly, d, c);
   if (!pl.ok) return fail(SK_ERR_UNSUPPORTED, "fast path does not cover this configuration");
   Packed pk{};
-  int rc = pack_roles(X, nx, lx, Y, ny, ly, d, symmetric != 0, pl, c, ws, ws_bytes, st, pk);
+  int rc = pack_roles(X, nx, lx, Y, ny, ly, d, pl, c, ws, ws_bytes, st, pk);
   if (rc) return rc;
-  Params P = base_params(pl, pk, lx);
+  Params P = base_params(pl, pk);
   P.nx = nx;
   P.ny = ny;
   P.tiles_y = (ny + pl.segs - 1) / pl.segs;
@@ -238,7 +271,7 @@ int fast_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t 
   P.K = K;
   P.ldk = ldk;
   P.levels = levels;
-  return launch(P, pl, c.n_levels, st);
+  return launch(P, pl, c.n_levels, c.order, st);
 }
 
 int fast_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
@@ -249,11 +282,11 @@ int fast_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
   if (!pl.ok) return fail(SK_ERR_UNSUPPORTED, "fast path does not cover this configuration");
   if (n <= 0) return SK_OK;
   Packed pk{};
-  int rc = pack_roles(X, n, l, X, n, l, d, true, pl, c, ws, ws_bytes, st, pk);
+  int rc = pack_roles(X, n, l, X, n, l, d, pl, c, ws, ws_bytes, st, pk);
   if (rc) return rc;
   // each CTA evaluates its segments' y against the same sequences as x and
   // keeps the diagonal: the same kernel and arithmetic as the Gram's diagonal
-  Params P = base_params(pl, pk, l);
+  Params P = base_params(pl, pk);
   P.nx = P.ny = n;
   P.tiles_y = (n + pl.segs - 1) / pl.segs;
   P.ntiles = P.tiles_y;
@@ -263,7 +296,7 @@ int fast_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
   P.diag_mode = 1;
   P.norm = SK_NORM_NONE;
   P.self_out = out;
-  return launch(P, pl, c.n_levels, st);
+  return launch(P, pl, c.n_levels, c.order, st);
 }
 
 }  // namespace sk

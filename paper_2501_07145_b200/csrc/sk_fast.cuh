@@ -13,27 +13,40 @@
 // Lane q of a segment owns C = 8 point-kernel columns g in [C*q, C*q + C) of
 // the pair's L_x x L_y grid and keeps, in registers, those columns' y points
 // and the column accumulators colacc_m(g) = sum_{i' < i} R_m(i', g) for levels
-// m = 1..M-1. Rows are streamed top to bottom, but lane q runs q steps
-// behind lane 0 (a wavefront). That skew turns the 2-D exclusive prefix
+// m = 1..M-1. Rows are streamed top to bottom, TWO rows (a row pair) per
+// step, and lane q runs q steps behind lane 0 (a wavefront). That skew turns
+// the 2-D exclusive prefix
 //   S_m(i, j) = sum_{i' < i, j' < j} R_m(i', j')
 // into a chain: lane q receives from lane q-1 (one __shfl_up per level per
-// step) the prefix of everything left of its columns for the SAME row, adds
+// row) the prefix of everything left of its columns for the SAME row, adds
 // its own colaccs serially, and passes the result on next step. Per cell and
-// level that is one FADD (scan) + one FFMA (colacc += A * S), i.e. the
+// level that is one FADD (scan) + one FFMA (accumulate), i.e. the
 // north-star flop model's 4 flops/level/cell, with the cross-lane scan cost
 // amortised over C cells.
+//
+// Row pairs: the point kernel of both rows is evaluated with packed
+// FFMA2 (fma.rn.f32x2): the x coordinates of the two rows form one 64-bit
+// register pair, reused across the C columns, times the column's y
+// coordinate as a broadcast scalar operand. That halves the issue slots of
+// the dominant stage at the same FP32-pipe cost (tools/microbench/
+// ffma2_rowpair.cu: 127.7 of 128 lane-FMAs/SM/clk), which leaves issue
+// bandwidth for the MUFU/SHFL/LDS work of the rest of the step. The level
+// recursion then runs row a, then row b.
 //
 // Pairs stream back to back: a segment keeps its y sequence and walks a
 // range of x sequences; each lane switches to the next x when its own row
 // counter wraps, so there is no wavefront fill/drain per pair. The level
 // sums of a finished pair arrive for free at the segment's last lane: at a
-// lane's first step of the next pair, the chain carries sum over all lanes of
-// sum_g colacc_m(g) = k_m (and k_M rides a separate chain).
+// lane's first step of the next pair, the row-a chain carries sum over all
+// lanes of sum_g colacc_m(g) = k_m (and k_M rides a separate chain). Row a of
+// that step is the new x's row 0, whose "increments" against the previous x
+// are discarded by the reset between rows a and b.
 //
 // Increments: lane q needs D(g) = G(i,g) - G(i-1,g) for g = C*q - 1, which
 // lane q-1 computed one step earlier; it arrives with the carries, so every
 // point-kernel value is computed exactly once. Columns beyond L_y repeat the
-// last y point (zero increments, A = 0), which is exact.
+// last y point, and an odd L_x repeats the last x point (zero increments,
+// A = 0), which is exact.
 //
 // Point kernel: x and y are pre-scaled (rbf: by sqrt(log2 e)/sigma) and
 // carry n = -|x'|^2/2, so G = exp2(min(<x',y'> + n_x + n_y, 0)) — the
@@ -46,21 +59,25 @@
 #pragma once
 
 #include "sk_common.cuh"
+#include "sk_geo_cells.cuh"
 
 namespace sk {
 namespace fast {
 
 constexpr int NWARPS = 8;
 constexpr int NTHREADS = NWARPS * 32;
-constexpr int C = 8;  // point-kernel columns per lane
 constexpr int NSLOT = 3;
 
+// floats per packed point of the y role / per packed row pair of the x role
+__host__ __device__ constexpr int y_stride(int D) { return D + 4; }
+__host__ __device__ constexpr int x_stride(int D) { return 2 * D + 4; }
+
 struct Params {
-  const float *xs;  // x role (Gram rows), packed [nx][lxp][DP]
-  const float *ys;  // y role (Gram columns), packed [ny][lyp][DP]
+  const float *xs;  // x role (Gram rows), packed row pairs [nx][lx2][2D+4]
+  const float *ys;  // y role (Gram columns), packed [ny][lyp][D+4]
   int64_t nx, ny;
-  int lx;        // x points per sequence (rows streamed per pair)
-  int lxp, lyp;  // packed point strides
+  int lx2;       // x row pairs per sequence (steps per pair)
+  int lyp;       // packed y point stride
   int sw;        // lanes per segment
   int segs;      // segments (y sequences) per CTA
   int rx;        // x sequences per tile
@@ -77,15 +94,36 @@ struct Params {
   // multi-panel (L_y > 256): the pair's columns are swept in npanel passes of
   // 256 columns; chain values cross panel boundaries through `carry`
   int npanel;
-  float *carry;  // [max_ctas * NWARPS][rx + 2 jobs][lx rows][nhp]
-  int nhp;       // floats per carry entry (NCA chain values, lastD, kout; padded to 4)
+  float *carry;  // [max_ctas * NWARPS][rx + 2 jobs][lx2 steps][nhp]
+  int nhp;       // floats per carry entry (2 x NCA chain values, 2 x lastD, kout; padded to 4)
   int max_ctas;  // grid size the carry buffer was sized for
 };
+
+typedef unsigned long long u64;
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+__device__ __forceinline__ u64 pack2(float lo, float hi) {
+  u64 d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+  return d;
+}
+__device__ __forceinline__ void unpack2(u64 v, float &lo, float &hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+// d = a * {b, b} + c  (ptxas folds the broadcast into FFMA2's scalar operand)
+__device__ __forceinline__ u64 ffma2_bc(u64 a, float b, u64 c) {
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(pack2(b, b)), "l"(c));
+  return d;
+}
+__device__ __forceinline__ u64 fadd2_bc(u64 a, float b) {
+  u64 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(pack2(b, b)));
+  return d;
 }
 
 __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gmem_src) {
@@ -102,14 +140,15 @@ __device__ __forceinline__ void stage_sequence(float *dst, const float *src, int
   cp_async_commit();
 }
 
+// Level values of pair (i, j) -> per-level output and/or normalised K entry.
+// ls = k_1..k_{M-1} (float chain totals), kout = k_M.
 template <int M>
 __device__ __forceinline__ void write_pair(const Params &P, int64_t i, int64_t j,
-                                           const float (&cout)[(M >= 2) ? M - 1 : 1],
-                                           float kout) {
+                                           const float *ls, float kout) {
   double lv[M + 1];
   lv[0] = 1.0;
 #pragma unroll
-  for (int m = 1; m < M; ++m) lv[m] = (double)cout[m - 1];
+  for (int m = 1; m < M; ++m) lv[m] = (double)ls[m - 1];
   lv[M] = (double)kout;
   if (P.diag_mode) {
     if (i == j) {
@@ -137,19 +176,141 @@ __device__ __forceinline__ void write_pair(const Params &P, int64_t i, int64_t j
   }
 }
 
-// Per-lane register state of one segment lane and the systolic step.
-template <int D, int M, bool LINEAR>
-struct LaneState {
-  static constexpr int DP = D + 4;
-  static constexpr int NCA = (M >= 2) ? M - 1 : 0;  // column-accumulated levels 1..M-1
-  static constexpr int NCR = (NCA > 0) ? NCA : 1;
+// ---------------------------------------------------------------------------
+// Point stage shared by the lane states: this lane's C y columns in
+// registers, the packed-FFMA2 point kernel of a row pair, and the double
+// difference (kernels.py:281) producing the increments of rows a and b.
+// ---------------------------------------------------------------------------
+template <int D, int C_, bool LINEAR>
+struct PointStage {
+  static constexpr int C = C_;
+  static constexpr int XP = x_stride(D);
+  static constexpr int YP = y_stride(D);
 
   float yv[C][D];
   float yn[C];
-  float colacc[NCR][C];
   float prevG[C];
-  float cout[NCR];
-  float kM, kout, lastD;
+  float lastDa, lastDb;
+  float ga[C], gb[C];  // point-kernel rows a, b of the current row pair
+
+  // this lane's columns of the packed y sequence (pre-scaled points, n-terms)
+  __device__ __forceinline__ void load_y(const float *__restrict__ yp) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+#pragma unroll
+      for (int k4 = 0; k4 < D / 4; ++k4) {
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(yp + c * YP) + k4);
+        yv[c][4 * k4 + 0] = v.x;
+        yv[c][4 * k4 + 1] = v.y;
+        yv[c][4 * k4 + 2] = v.z;
+        yv[c][4 * k4 + 3] = v.w;
+      }
+      yn[c] = LINEAR ? 0.f : __ldg(yp + c * YP + D);
+      prevG[c] = 0.f;
+    }
+    lastDa = lastDb = 0.f;
+  }
+
+  // Point kernel of rows a, b of the row pair at `xptr` (packed FFMA2) -> ga, gb.
+  __device__ __forceinline__ void point(const float *__restrict__ xptr) {
+    u64 acc[C];
+    if (LINEAR) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[c] = 0ull;
+    } else {
+      const u64 xn2 = *reinterpret_cast<const u64 *>(xptr + 2 * D);
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[c] = fadd2_bc(xn2, yn[c]);
+    }
+    const float4 *xr = reinterpret_cast<const float4 *>(xptr);
+#pragma unroll
+    for (int k2 = 0; k2 < D / 2; ++k2) {
+      const float4 v = xr[k2];  // {x_a[2k2], x_b[2k2], x_a[2k2+1], x_b[2k2+1]}
+      const u64 p0 = pack2(v.x, v.y);
+      const u64 p1 = pack2(v.z, v.w);
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[c] = ffma2_bc(p0, yv[c][2 * k2], acc[c]);
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[c] = ffma2_bc(p1, yv[c][2 * k2 + 1], acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      float lo, hi;
+      unpack2(acc[c], lo, hi);
+      if (LINEAR) {
+        ga[c] = lo;
+        gb[c] = hi;
+      } else {
+        ga[c] = ex2_approx(fminf(lo, 0.f));
+        gb[c] = ex2_approx(fminf(hi, 0.f));
+      }
+    }
+  }
+
+  // A = D(g) - D(g-1), D = G(r,.) - G(r-1,.). dla/dlb: D of the column left
+  // of this lane (lane q-1's last column, or the previous panel's);
+  // zero_left: column -1 does not exist (A = 0).
+  // Linear kind: both roles are packed as increments (pack kernels), so the
+  // point kernel already is A = <dx_i, dy_j> (kernels.py:281 is bilinear),
+  // without the cancellation of differencing the point Gram in FP32.
+  __device__ __forceinline__ void increments(float dla, float dlb, bool zero_left, float (&aa)[C],
+                                             float (&ab)[C]) {
+    if constexpr (LINEAR) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        aa[c] = ga[c];
+        ab[c] = gb[c];
+      }
+      return;
+    }
+    float dva[C], dvb[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      dva[c] = ga[c] - prevG[c];
+      dvb[c] = gb[c] - ga[c];
+      prevG[c] = gb[c];
+    }
+    aa[0] = zero_left ? 0.f : dva[0] - dla;
+    ab[0] = zero_left ? 0.f : dvb[0] - dlb;
+#pragma unroll
+    for (int c = 1; c < C; ++c) {
+      aa[c] = dva[c] - dva[c - 1];
+      ab[c] = dvb[c] - dvb[c - 1];
+    }
+    lastDa = dva[C - 1];
+    lastDb = dvb[C - 1];
+  }
+};
+
+// Receive chain values from lane q-1 (its previous step); the segment head
+// takes zeros, or the previous panel's carries `hin[k]` when from_buf.
+template <int N>
+__device__ __forceinline__ void chain_in(const float (&out)[N], float (&in)[N], int n, int sw,
+                                         bool first_lane, bool from_buf, const float *hin) {
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    if (k < n) {
+      const float v = __shfl_up_sync(0xffffffffu, out[k], 1, sw);
+      in[k] = first_lane ? (from_buf ? hin[k] : 0.f) : v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Order p = 1 lane state (C = 8 columns per lane).
+// ---------------------------------------------------------------------------
+template <int D, int M_, bool LINEAR>
+struct LaneState1 : PointStage<D, 8, LINEAR> {
+  using Base = PointStage<D, 8, LINEAR>;
+  using Base::C;
+  static constexpr int M = M_;
+  static constexpr int NCA = (M >= 2) ? M - 1 : 0;  // column-accumulated levels 1..M-1
+  static constexpr int NCR = (NCA > 0) ? NCA : 1;
+  static constexpr int NHM = 2 * NCA + 3;  // carry entry: couta, coutb, lastDa, lastDb, kout
+
+  float colacc[NCR][C];
+  float couta[NCR], coutb[NCR];
+  float kM, kout;
 
   __device__ __forceinline__ void reset_pair() {
 #pragma unroll
@@ -159,77 +320,30 @@ struct LaneState {
     }
     kM = 0.f;
   }
-
-  // One row of this lane's C columns. KCHAIN: also run the level-M chain
-  // (only needed while some lane of the segment is at a pair boundary).
-  //  MULTI: the chain head takes its inputs from `hin` (the previous panel's
-  //         carries for this row) when head_buf, instead of zeros
-  template <bool KCHAIN, bool MULTI>
-  __device__ __forceinline__ void step(const float *__restrict__ xptr, int sw, bool first_lane,
-                                       const float *hin, bool head_buf) {
-    constexpr unsigned FULL = 0xffffffffu;
-    const bool from_buf = MULTI && head_buf;
-    // (a) chain values produced by lane q-1 on the previous step
-    float dl_raw = __shfl_up_sync(FULL, lastD, 1, sw);
-    float cin[NCR];
+  __device__ __forceinline__ void reset_panel() {
+    reset_pair();
+    kout = 0.f;
+#pragma unroll
+    for (int m = 0; m < NCR; ++m) couta[m] = coutb[m] = 0.f;
+  }
+  // level sums k_1..k_{M-1} of the pair that just completed (valid at the
+  // segment's last lane at its boundary step), and k_M = kout
+  __device__ __forceinline__ const float *level_sums() const { return couta; }
+  __device__ __forceinline__ void store_carry(float *dst) const {
 #pragma unroll
     for (int m = 0; m < NCA; ++m) {
-      const float v = __shfl_up_sync(FULL, cout[m], 1, sw);
-      cin[m] = first_lane ? (from_buf ? hin[m] : 0.f) : v;
+      dst[m] = couta[m];
+      dst[NCA + m] = coutb[m];
     }
-    if (from_buf && first_lane) dl_raw = hin[NCA];
-    if (KCHAIN) {
-      const float kin = __shfl_up_sync(FULL, kout, 1, sw);
-      kout = (first_lane ? (from_buf ? hin[NCA + 1] : 0.f) : kin) + kM;  // complete at a boundary
-    }
+    dst[2 * NCA] = this->lastDa;
+    dst[2 * NCA + 1] = this->lastDb;
+    dst[2 * NCA + 2] = kout;
+  }
 
-    // (b) point-kernel row for this lane's columns
-    float g[C];
-    {
-      float acc[C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) acc[c] = yn[c];
-      const float4 *xr = reinterpret_cast<const float4 *>(xptr);
-#pragma unroll
-      for (int k4 = 0; k4 < D / 4; ++k4) {
-        const float4 xv = xr[k4];
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-          acc[c] = fmaf(xv.x, yv[c][4 * k4 + 0], acc[c]);
-          acc[c] = fmaf(xv.y, yv[c][4 * k4 + 1], acc[c]);
-          acc[c] = fmaf(xv.z, yv[c][4 * k4 + 2], acc[c]);
-          acc[c] = fmaf(xv.w, yv[c][4 * k4 + 3], acc[c]);
-        }
-      }
-      if (LINEAR) {
-#pragma unroll
-        for (int c = 0; c < C; ++c) g[c] = acc[c];
-      } else {
-        const float xn = xptr[D];
-#pragma unroll
-        for (int c = 0; c < C; ++c) g[c] = ex2_approx(fminf(acc[c] + xn, 0.f));
-      }
-    }
-
-    // (c) increments of the previous DP row: A = D(g) - D(g-1), D = G(r,.) - G(r-1,.)
-    float a[C];
-    {
-      float dv[C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        dv[c] = g[c] - prevG[c];
-        prevG[c] = g[c];
-      }
-      // column -1 of the first panel does not exist (A = 0); a later panel's
-      // head gets D of the previous panel's last column through the carry
-      const float dl = (first_lane && !from_buf) ? dv[0] : dl_raw;
-      a[0] = dv[0] - dl;
-#pragma unroll
-      for (int c = 1; c < C; ++c) a[c] = dv[c] - dv[c - 1];
-      lastD = dv[C - 1];
-    }
-
-    // (d) level recursion along the row (p = 1): R_m = A * S(R_{m-1})
+  // Level recursion of one row (p = 1): R_m = A * S(R_{m-1}); cin = the
+  // chain's prefix left of this lane, cout = prefix including this lane.
+  __device__ __forceinline__ void row(const float (&a)[C], const float (&cin)[NCR],
+                                      float (&cout)[NCR]) {
     if constexpr (M == 1) {
 #pragma unroll
       for (int c = 0; c < C; ++c) kM += a[c];
@@ -254,17 +368,157 @@ struct LaneState {
       for (int m = 0; m < NCA; ++m) cout[m] = sc[m];
     }
   }
+
+  // One row pair (at `xptr`) of this lane's C columns. (Software-pipelining
+  // the next row pair's point kernel into this step's recursion was measured
+  // slower: 255 registers, 57% vs 62% of the FP32 roofline at c3.)
+  //  KCHAIN: also run the level-M chain (only needed while some lane of the
+  //          segment is at a pair boundary).
+  //  MULTI:  the chain head takes its inputs from `hin` (the previous panel's
+  //          carries for this row pair) when head_buf, instead of zeros.
+  //  BCHK:   `boundary` may be true: row a starts a new pair, so the pair
+  //          state is reset between rows a and b.
+  template <bool KCHAIN, bool MULTI, bool BCHK>
+  __device__ __forceinline__ void step(const float *__restrict__ xptr, int sw, bool first_lane,
+                                       const float *hin, bool head_buf, bool boundary) {
+    const bool from_buf = MULTI && head_buf;
+    // (a) chain values produced by lane q-1 on the previous step
+    float dla = __shfl_up_sync(0xffffffffu, this->lastDa, 1, sw);
+    float dlb = __shfl_up_sync(0xffffffffu, this->lastDb, 1, sw);
+    float cina[NCR], cinb[NCR];
+    chain_in(couta, cina, NCA, sw, first_lane, from_buf, hin);
+    chain_in(coutb, cinb, NCA, sw, first_lane, from_buf, hin + NCA);
+    if (from_buf && first_lane) {
+      dla = hin[2 * NCA];
+      dlb = hin[2 * NCA + 1];
+    }
+    if (KCHAIN) {
+      const float kin = __shfl_up_sync(0xffffffffu, kout, 1, sw);
+      kout = (first_lane ? (from_buf ? hin[2 * NCA + 2] : 0.f) : kin) + kM;  // complete at a boundary
+    }
+    // (b) point kernel of rows a, b; (c) increments
+    this->point(xptr);
+    float aa[C], ab[C];
+    this->increments(dla, dlb, first_lane && !from_buf, aa, ab);
+    // (d) level recursion, row a then row b
+    row(aa, cina, couta);
+    if (BCHK && boundary) reset_pair();
+    row(ab, cinb, coutb);
+  }
 };
 
-template <int D, int M, bool LINEAR, bool MULTI>
-__global__ void __launch_bounds__(NTHREADS, 1) gram_p1_kernel(const Params P) {
-  static_assert(D % 4 == 0, "D must be a multiple of 4");
-  static_assert(M >= 1, "M >= 1");
-  using LS = LaneState<D, M, LINEAR>;
-  constexpr int DP = LS::DP;
+// ---------------------------------------------------------------------------
+// General order 1 < p <= M (the geometric kernel at p = M), C = 4 columns
+// per lane. The reference's recursion (kernels.py:179-199):
+//   R'[0,0] = A S(C),                 C = sum_{q,r} R[q,r]
+//   R'[q,0] = A/(q+1) E_j(sum_r R[q-1,r])
+//   R'[0,r] = A/(r+1) E_i(sum_q R[q,r-1])
+//   R'[q,r] = A/((q+1)(r+1)) R[q-1,r-1]
+// is run per cell on factorial-scaled states Rs[q,r] = (q+1)!(r+1)! R[q,r],
+// which turns every state update into one multiply by A:
+//   Rs'[0,0] = A S(C),  Rs'[q,0] = A e_q,  Rs'[0,r] = A f_r,  Rs'[q,r] = A Rs[q-1,r-1]
+// with the scaled prefixes e_q = E_j(rs[q-1]), f_r = E_i(cs[r-1]) of the row
+// and column sums rs[q] = sum_r Rs[q,r]/(r+1)!, cs[r] = sum_q Rs[q,r]/(q+1)!,
+// and C = sum_q rs[q]/(q+1)!. S and E_i are column accumulators (colS, colE)
+// plus, for S, the cross-lane chain; E_j is a pure row prefix: a running sum
+// along the lane's columns plus a cross-lane chain, exactly like S.
+// ---------------------------------------------------------------------------
+template <int D, int M_, int P, bool LINEAR>
+struct LaneStateG : PointStage<D, 4, LINEAR> {
+  using Base = PointStage<D, 4, LINEAR>;
+  using Base::C;
+  using Cell = GeoCell<M_, P>;  // generated straight-line cell (sk_geo_cells.cuh)
+  static constexpr int M = M_;
+  static_assert(P >= 2 && P <= M, "general-order lane state needs 2 <= p <= M");
+  static constexpr int NS = Cell::NS;   // S chains / colS: C_m of levels 1..M-1
+  static constexpr int NE = Cell::NE;   // E chains / colE
+  static constexpr int NCH = NS + NE;   // chain values per row
+  static constexpr int NHM = 2 * NCH + 3;
+
+  float colS[C][NS];
+  float colE[C][NE];
+  float cha[NCH], chb[NCH];  // chain outputs of rows a, b: [S (NS) | E (NE)]
+  float kM, kout;
+
+  __device__ __forceinline__ void reset_pair() {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+#pragma unroll
+      for (int m = 0; m < NS; ++m) colS[c][m] = 0.f;
+#pragma unroll
+      for (int k = 0; k < NE; ++k) colE[c][k] = 0.f;
+    }
+    kM = 0.f;
+  }
+  __device__ __forceinline__ void reset_panel() {
+    reset_pair();
+    kout = 0.f;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) cha[k] = chb[k] = 0.f;
+  }
+  __device__ __forceinline__ const float *level_sums() const { return cha; }
+  __device__ __forceinline__ void store_carry(float *dst) const {
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      dst[k] = cha[k];
+      dst[NCH + k] = chb[k];
+    }
+    dst[2 * NCH] = this->lastDa;
+    dst[2 * NCH + 1] = this->lastDb;
+    dst[2 * NCH + 2] = kout;
+  }
+
+  // Level recursion of one row. cin/cout: [S prefixes | E prefixes].
+  __device__ __forceinline__ void row(const float (&a)[C], const float (&cin)[NCH],
+                                      float (&cout)[NCH]) {
+    float sc[NS], ec[NE];
+#pragma unroll
+    for (int m = 0; m < NS; ++m) sc[m] = cin[m];
+#pragma unroll
+    for (int k = 0; k < NE; ++k) ec[k] = cin[NS + k];
+#pragma unroll
+    for (int c = 0; c < C; ++c) Cell::cell(a[c], sc, ec, colS[c], colE[c], kM);
+#pragma unroll
+    for (int m = 0; m < NS; ++m) cout[m] = sc[m];
+#pragma unroll
+    for (int k = 0; k < NE; ++k) cout[NS + k] = ec[k];
+  }
+
+  template <bool KCHAIN, bool MULTI, bool BCHK>
+  __device__ __forceinline__ void step(const float *__restrict__ xptr, int sw, bool first_lane,
+                                       const float *hin, bool head_buf, bool boundary) {
+    const bool from_buf = MULTI && head_buf;
+    float dla = __shfl_up_sync(0xffffffffu, this->lastDa, 1, sw);
+    float dlb = __shfl_up_sync(0xffffffffu, this->lastDb, 1, sw);
+    float cina[NCH], cinb[NCH];
+    chain_in(cha, cina, NCH, sw, first_lane, from_buf, hin);
+    chain_in(chb, cinb, NCH, sw, first_lane, from_buf, hin + NCH);
+    if (from_buf && first_lane) {
+      dla = hin[2 * NCH];
+      dlb = hin[2 * NCH + 1];
+    }
+    if (KCHAIN) {
+      const float kin = __shfl_up_sync(0xffffffffu, kout, 1, sw);
+      kout = (first_lane ? (from_buf ? hin[2 * NCH + 2] : 0.f) : kin) + kM;
+    }
+    this->point(xptr);
+    float aa[C], ab[C];
+    this->increments(dla, dlb, first_lane && !from_buf, aa, ab);
+    row(aa, cina, cha);
+    if (BCHK && boundary) reset_pair();
+    row(ab, cinb, chb);
+  }
+};
+
+template <class LS, bool MULTI>
+__global__ void __launch_bounds__(NTHREADS, 1) gram_kernel(const Params P) {
+  constexpr int M = LS::M;
+  constexpr int C = LS::C;
+  constexpr int XP = LS::XP;
+  constexpr int YP = LS::YP;
   extern __shared__ __align__(16) float smem[];
-  const int lx = P.lx;
-  const int slot_floats = lx * DP;
+  const int lx2 = P.lx2;
+  const int slot_floats = lx2 * XP;
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -293,149 +547,119 @@ __global__ void __launch_bounds__(NTHREADS, 1) gram_p1_kernel(const Params P) {
     const int64_t jj = jvalid ? j : P.ny - 1;
 
     // carry region of this warp (multi-panel only)
-    float *cbuf = MULTI ? P.carry + ((size_t)(blockIdx.x * NWARPS + warp) * (P.rx + 2)) * lx * P.nhp
+    float *cbuf = MULTI ? P.carry + ((size_t)(blockIdx.x * NWARPS + warp) * (P.rx + 2)) * lx2 * P.nhp
                         : nullptr;
     const int npanel = MULTI ? P.npanel : 1;
     for (int pnl = 0; pnl < npanel; ++pnl) {
       // this lane's y columns of panel pnl (pre-scaled points and their n-terms)
-      {
-        const float *yp = P.ys + ((size_t)jj * P.lyp + (size_t)pnl * 32 * C + (size_t)q * C) * DP;
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-#pragma unroll
-          for (int k4 = 0; k4 < D / 4; ++k4) {
-            const float4 v = __ldg(reinterpret_cast<const float4 *>(yp + c * DP) + k4);
-            st.yv[c][4 * k4 + 0] = v.x;
-            st.yv[c][4 * k4 + 1] = v.y;
-            st.yv[c][4 * k4 + 2] = v.z;
-            st.yv[c][4 * k4 + 3] = v.w;
-          }
-          st.yn[c] = LINEAR ? 0.f : __ldg(yp + c * DP + D);
-          st.prevG[c] = 0.f;
-        }
-      }
-      st.reset_pair();
-      st.kout = st.lastD = 0.f;
-#pragma unroll
-      for (int m = 0; m < LS::NCR; ++m) st.cout[m] = 0.f;
+      st.load_y(P.ys + ((size_t)jj * P.lyp + (size_t)pnl * 32 * C + (size_t)q * C) * YP);
+      st.reset_panel();
       const bool head_buf = MULTI && pnl > 0;          // chain inputs from the previous panel
       const bool tail_buf = MULTI && pnl < npanel - 1;  // chain outputs for the next panel
       const bool last_panel = pnl == npanel - 1;
 
       __syncthreads();  // previous readers are done with the ring (and the carries are visible)
-      stage_sequence(smem, P.xs + (size_t)x0 * P.lxp * DP, slot_floats);
+      stage_sequence(smem, P.xs + (size_t)x0 * lx2 * XP, slot_floats);
 
-      // head inputs, prefetched one step ahead (lane 0 reads job e, row s)
-      constexpr int NHM = LS::NCA + 2;
+      // head inputs, prefetched one step ahead (lane 0 reads job e, row pair s)
+      constexpr int NHM = LS::NHM;
       float hcur[NHM], hnext[NHM];
 #pragma unroll
       for (int k = 0; k < NHM; ++k) hcur[k] = hnext[k] = 0.f;
-      auto load_head = [&](float (&h)[NHM], int64_t job, int row) {
+      auto load_head = [&](float (&h)[NHM], int64_t job, int rp) {
         if (head_buf && first_lane) {
-          const float *src = cbuf + ((size_t)job * lx + row) * P.nhp;
+          const float *src = cbuf + ((size_t)job * lx2 + rp) * P.nhp;
 #pragma unroll
           for (int k = 0; k < NHM; ++k) h[k] = src[k];
         }
       };
-      auto store_tail = [&](int64_t job, int row) {
-        if (tail_buf && last_lane && job >= 0) {
-          float *dst = cbuf + ((size_t)job * lx + row) * P.nhp;
-#pragma unroll
-          for (int m = 0; m < LS::NCA; ++m) dst[m] = st.cout[m];
-          dst[LS::NCA] = st.lastD;
-          dst[LS::NCA + 1] = st.kout;
-        }
+      auto store_tail = [&](int64_t job, int rp) {
+        if (tail_buf && last_lane && job >= 0)
+          st.store_carry(cbuf + ((size_t)job * lx2 + rp) * P.nhp);
       };
       load_head(hcur, 0, 0);
 
       // Epoch e streams x_{x0+e}: lane q starts that pair at step s = q (its
-      // row 0) and spends steps s < q finishing pair e-1. So pair boundaries
-      // only occur in steps s < sw ("phase A"); steps s >= sw are branch-free.
+      // row pair 0) and spends steps s < q finishing pair e-1. So pair
+      // boundaries only occur in steps s < sw ("phase A"); steps s >= sw are
+      // branch-free.
       for (int64_t e = 0; e <= njobs; ++e) {
         cp_async_wait_all();
         __syncthreads();
         if (e + 1 < njobs)
           stage_sequence(smem + ((e + 1) % NSLOT) * slot_floats,
-                         P.xs + (size_t)(x0 + e + 1) * P.lxp * DP, slot_floats);
+                         P.xs + (size_t)(x0 + e + 1) * lx2 * XP, slot_floats);
         const float *cur = smem + (e % NSLOT) * slot_floats;
         // before its first pair a lane idles on rows of x_{x0} (slot 0)
         const float *prev = (e == 0) ? smem : smem + ((e + NSLOT - 1) % NSLOT) * slot_floats;
-        const int steps = (e < njobs) ? lx : sw;
+        const int steps = (e < njobs) ? lx2 : sw;
         const int nA = min(sw, steps);
         for (int s = 0; s < nA; ++s) {
           if (MULTI) load_head(hnext, s + 1 < steps ? e : e + 1, s + 1 < steps ? s + 1 : 0);
-          const float *xp = (s < q) ? prev + (lx - q + s) * DP : cur + (s - q) * DP;
-          st.template step<true, MULTI>(xp, sw, first_lane, hcur, head_buf);
+          const float *xp = (s < q) ? prev + (lx2 - q + s) * XP : cur + (s - q) * XP;
+          st.template step<true, MULTI, true>(xp, sw, first_lane, hcur, head_buf, s == q);
           if (MULTI) {
-            // the segment's last lane is at (job, row) = (e, s - q) or (e - 1, lx - q + s)
+            // the segment's last lane is at (job, pair) = (e, s - q) or (e - 1, lx2 - q + s)
             if (s >= q)
               store_tail(e, s - q);
             else
-              store_tail(e - 1, lx - q + s);
+              store_tail(e - 1, lx2 - q + s);
           }
           if (s == q) {  // this lane's pair boundary: pair e-1 is complete
             if (last_panel && last_lane && e >= 1 && jvalid)
-              write_pair<M>(P, x0 + e - 1, j, st.cout, st.kout);
-            st.reset_pair();
+              write_pair<M>(P, x0 + e - 1, j, st.level_sums(), st.kout);
           }
           if (MULTI) {
 #pragma unroll
             for (int k = 0; k < NHM; ++k) hcur[k] = hnext[k];
           }
         }
-        const float *xp = cur + (nA - q) * DP;
-#pragma unroll 2
+        const float *xp = cur + (nA - q) * XP;
+#pragma unroll 1
         for (int s = nA; s < steps; ++s) {
           if (MULTI) load_head(hnext, s + 1 < steps ? e : e + 1, s + 1 < steps ? s + 1 : 0);
-          st.template step<false, MULTI>(xp, sw, first_lane, hcur, head_buf);
+          st.template step<false, MULTI, false>(xp, sw, first_lane, hcur, head_buf, false);
           if (MULTI) {
             store_tail(e, s - q);
 #pragma unroll
             for (int k = 0; k < NHM; ++k) hcur[k] = hnext[k];
           }
-          xp += DP;
+          xp += XP;
         }
       }
     }
   }
 }
 
-// Pack (N, L, d) float64 -> [N][Lp][DP] float32 with pre-scaled coordinates,
-// zero-padded channels, the n-term in column D, and points beyond L
-// repeating the last point.
-__global__ void pack_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
-                            int64_t Lp, int D, int DP, double coord_scale, int with_norm,
-                            float *__restrict__ out);
+// Pack (N, L, d) float64 into the kernel layouts with pre-scaled coordinates,
+// zero-padded channels and the n-term (from the rounded coordinates):
+//  y role: [N][Lp][D+4], point p = min(p, L-1), n-term at column D.
+//  x role: [N][Lp2][2D+4] row pairs, rows (2t, 2t+1) interleaved per
+//          channel, n-terms at 2D, 2D+1; rows beyond L repeat the last point.
+//  incr = 1 (linear kind): each point is replaced by the increment ending
+//  there, x_p - x_{p-1} (0 for p = 0 and beyond L), computed in float64.
+__global__ void pack_y_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
+                              int64_t Lp, int D, double coord_scale, int incr,
+                              float *__restrict__ out);
+__global__ void pack_x_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
+                              int64_t Lp2, int D, double coord_scale, int incr,
+                              float *__restrict__ out);
 
-int launch_d4(const Params &, int M, int linear, size_t smem, cudaStream_t st);
-int launch_d8(const Params &, int M, int linear, size_t smem, cudaStream_t st);
-int launch_d16(const Params &, int M, int linear, size_t smem, cudaStream_t st);
+int launch_d4(const Params &, int M, int order, int linear, size_t smem, cudaStream_t st);
+int launch_d8(const Params &, int M, int order, int linear, size_t smem, cudaStream_t st);
+int launch_d16(const Params &, int M, int order, int linear, size_t smem, cudaStream_t st);
 
-// Instantiation helper shared by the per-D translation units.
-template <int D>
-int launch_impl(const Params &P, int M, int linear, size_t smem, cudaStream_t st) {
+// Compiled (n_levels, order) combinations: order 1 with n_levels 1..8, and
+// the geometric kernel order = n_levels for n_levels 2..5.
+__host__ __device__ constexpr bool fast_orders_supported(int M, int order) {
+  return (order == 1 && M >= 1 && M <= 8) || (order == M && M >= 2 && M <= 5);
+}
+__host__ __device__ constexpr int columns_per_lane(int order) { return order == 1 ? 8 : 4; }
+
+template <class LS>
+int launch_kernel(const Params &P, size_t smem, cudaStream_t st) {
   using K = void (*)(const Params);
-  K k = nullptr;
-#define SK_CASE(MM)                                                                       \
-  case MM:                                                                                \
-    if (P.npanel > 1)                                                                     \
-      k = linear ? gram_p1_kernel<D, MM, true, true> : gram_p1_kernel<D, MM, false, true>;  \
-    else                                                                                  \
-      k = linear ? gram_p1_kernel<D, MM, true, false> : gram_p1_kernel<D, MM, false, false>; \
-    break;
-  switch (M) {
-    SK_CASE(1)
-    SK_CASE(2)
-    SK_CASE(3)
-    SK_CASE(4)
-    SK_CASE(5)
-    SK_CASE(6)
-    SK_CASE(7)
-    SK_CASE(8)
-    default:
-      return fail(SK_ERR_UNSUPPORTED, "fast path: n_levels outside 1..8");
-  }
-#undef SK_CASE
+  const K k = P.npanel > 1 ? gram_kernel<LS, true> : gram_kernel<LS, false>;
   SK_CHECK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   SK_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NTHREADS, smem));
@@ -447,6 +671,39 @@ int launch_impl(const Params &P, int M, int linear, size_t smem, cudaStream_t st
   k<<<grid, NTHREADS, smem, st>>>(P);
   SK_CHECK_LAUNCH();
   return SK_OK;
+}
+
+template <int D, bool LIN>
+int launch_impl_lin(const Params &P, int M, int order, size_t smem, cudaStream_t st) {
+  if (order == 1) {
+    switch (M) {
+      case 1: return launch_kernel<LaneState1<D, 1, LIN>>(P, smem, st);
+      case 2: return launch_kernel<LaneState1<D, 2, LIN>>(P, smem, st);
+      case 3: return launch_kernel<LaneState1<D, 3, LIN>>(P, smem, st);
+      case 4: return launch_kernel<LaneState1<D, 4, LIN>>(P, smem, st);
+      case 5: return launch_kernel<LaneState1<D, 5, LIN>>(P, smem, st);
+      case 6: return launch_kernel<LaneState1<D, 6, LIN>>(P, smem, st);
+      case 7: return launch_kernel<LaneState1<D, 7, LIN>>(P, smem, st);
+      case 8: return launch_kernel<LaneState1<D, 8, LIN>>(P, smem, st);
+      default: break;
+    }
+  } else if (order == M) {
+    switch (M) {
+      case 2: return launch_kernel<LaneStateG<D, 2, 2, LIN>>(P, smem, st);
+      case 3: return launch_kernel<LaneStateG<D, 3, 3, LIN>>(P, smem, st);
+      case 4: return launch_kernel<LaneStateG<D, 4, 4, LIN>>(P, smem, st);
+      case 5: return launch_kernel<LaneStateG<D, 5, 5, LIN>>(P, smem, st);
+      default: break;
+    }
+  }
+  return fail(SK_ERR_UNSUPPORTED, "fast path: (n_levels, order) not compiled");
+}
+
+// Instantiation helper shared by the per-D translation units.
+template <int D>
+int launch_impl(const Params &P, int M, int order, int linear, size_t smem, cudaStream_t st) {
+  return linear ? launch_impl_lin<D, true>(P, M, order, smem, st)
+                : launch_impl_lin<D, false>(P, M, order, smem, st);
 }
 
 }  // namespace fast

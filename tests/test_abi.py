@@ -59,8 +59,8 @@ def test_workspace_sizes():
     c3 = _native.config_struct(KernelConfig(n_levels=5, normalization="levelwise"))
     n, L, d = 8192, 256, 16
     ws = lib.sk_workspace_bytes(n, L, n, L, d, c3)
-    # packed fp32 X (x role) + Y (y role, 20 floats per point)
-    assert ws == 2 * n * L * 20 * 4
+    # packed fp32 x role (row pairs, 2*16+4 floats) + y role (16+4 floats per point)
+    assert ws == n * (L // 2) * 36 * 4 + n * L * 20 * 4
     f64 = _native.config_struct(KernelConfig(n_levels=3, order=2), "fp64")
     assert lib.sk_workspace_bytes(4, 6, 5, 7, 2, f64) > 0
 

@@ -197,3 +197,57 @@ def test_full_c3_prefix_block(gram_cases):
     K = sig_kernel_gram(X, Y, cfg=pkg_config(c))
     assert _rel(K[:4, :4], K_ref) <= TOL_NORM
     assert np.isfinite(K).all() and np.abs(K).max() <= 1.0 + 1e-6
+
+
+def _scaled_err(K, R):
+    """Relative error with entries that cancel to ~0 judged against 1e-3 of the largest."""
+    K, R = np.asarray(K), np.asarray(R)
+    scale = np.maximum(np.abs(R), 1e-3 * np.abs(R).max())
+    return float((np.abs(K - R) / scale).max())
+
+
+@pytest.mark.parametrize("M", [2, 3, 4, 5])
+@pytest.mark.parametrize("kind", ["rbf", "linear"])
+def test_geometric_order_fused(M, kind):
+    """order = n_levels (geometric) runs on the fused FP32 kernel (kernels.py:179-199)."""
+    X = gen_brownian(7, 60, 5, SeedStream(21)).data
+    Y = gen_brownian(6, 45, 5, SeedStream(22)).data
+    sp = O.static_params(kind)
+    for norm, tol in (("none", TOL_RAW), ("levelwise", TOL_NORM)):
+        cfg = KernelConfig(static=StaticKernelSpec(kind=kind), n_levels=M, order=M,
+                           normalization=norm)
+        fused = not (kind == "linear" and norm != "none")  # see plan_for (sk_fast.cu)
+        assert uses_fast_path(60, 45, 5, cfg) == fused and uses_fast_path(45, 60, 5, cfg) == fused
+        if not fused:
+            tol = 1e-10
+        R = O.gram(X, Y, sp=sp, M=M, p=M, normalization=norm)
+        assert _scaled_err(sig_kernel_gram(X, Y, cfg=cfg), R) <= tol, (M, kind, norm)
+        assert _scaled_err(sig_kernel_gram(Y, X, cfg=cfg), R.T) <= tol, (M, kind, norm)
+
+
+def test_geometric_multi_panel_symmetric():
+    """L > 128: the general-order kernel's 128-column panels chained through the carry."""
+    X = gen_brownian(9, 300, 3, SeedStream(23)).data
+    Y = gen_brownian(5, 140, 3, SeedStream(24)).data
+    for norm, tol in (("none", TOL_RAW), ("levelwise", TOL_NORM)):
+        cfg = KernelConfig(n_levels=4, order=4, normalization=norm)
+        assert uses_fast_path(300, 300, 3, cfg)
+        R = O.gram(X, Y, M=4, p=4, normalization=norm)
+        assert _scaled_err(sig_kernel_gram(X, Y, cfg=cfg), R) <= tol, norm
+        assert _scaled_err(sig_kernel_gram(Y, X, cfg=cfg), R.T) <= tol, norm
+    cfg = KernelConfig(n_levels=5, order=5, normalization="levelwise")
+    K = sig_kernel_gram(X, cfg=cfg)
+    assert np.array_equal(K, K.T) and np.array_equal(np.diag(K), np.ones(9))
+    assert _scaled_err(K, O.gram(X, None, M=5, p=5, normalization="levelwise")) <= TOL_NORM
+
+
+def test_c2_shapes_fused_vs_fp64():
+    """c2 (L=128, d=8, M=p=5) sub-block: fused FP32 geometric kernel vs the float64 kernel."""
+    X = gen_brownian(10, 128, 8, SeedStream(1)).data
+    Y = gen_brownian(9, 128, 8, SeedStream(2)).data
+    for norm, tol in (("none", TOL_RAW), ("levelwise", TOL_NORM)):
+        cfg = KernelConfig(n_levels=5, order=5, normalization=norm)
+        assert uses_fast_path(128, 128, 8, cfg)
+        K32 = sig_kernel_gram(X, Y, cfg=cfg)
+        K64 = sig_kernel_gram(X, Y, cfg=cfg, precision="fp64")
+        assert _rel(K32, K64) <= tol, norm
