@@ -43,7 +43,12 @@ def test_fast_path_selection():
     assert lib.sk_fast_path(128, 128, 16, lin) == 1
     assert lib.sk_fast_path(128, 128, 128, lin) == 0        # d > 16: float64 path (for now)
     geo = _native.config_struct(KernelConfig(n_levels=5, order=5))
-    assert lib.sk_fast_path(128, 128, 8, geo) == 0          # p > 1
+    assert lib.sk_fast_path(128, 128, 8, geo) == 1          # geometric p = M (c2)
+    mid = _native.config_struct(KernelConfig(n_levels=5, order=3))
+    assert lib.sk_fast_path(128, 128, 8, mid) == 0          # 1 < p < M: float64 kernel
+    lgeo = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="linear"), n_levels=4,
+                                              order=4, normalization="levelwise"))
+    assert lib.sk_fast_path(64, 64, 4, lgeo) == 0           # normalised linear p > 1: float64
     f64 = _native.config_struct(KernelConfig(n_levels=5), "fp64")
     assert lib.sk_fast_path(256, 256, 16, f64) == 0
     mat = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="matern32")))
