@@ -1,5 +1,6 @@
 # Builds the in-tree sm_100a library paper_2501_07145_b200/_lib/libsigkern_b200.so.
-# cudart is linked statically so the .so loads (symbol check) without a GPU.
+# cudart is linked statically so the .so loads (symbol check) without a GPU;
+# cuBLAS (the GEMM-fed large-d path) is linked dynamically.
 NVCC      ?= nvcc
 ARCH      ?= -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   ?= -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
@@ -21,7 +22,7 @@ $(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
 
 $(LIB): $(OBJS)
 	@mkdir -p $(OUT_DIR)
-	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS) -Xcompiler -fvisibility=hidden
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS) -Xcompiler -fvisibility=hidden -lcublas
 
 clean:
 	rm -rf build $(LIB)

@@ -73,21 +73,23 @@ const char *sk_last_error(void) { return g_error.c_str(); }
 
 int sk_fast_path(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config *cfg) {
   if (!cfg) return 0;
-  return fast_supported(lx, ly, d, *cfg) ? 1 : 0;
+  return path_of(lx, ly, d, *cfg);
 }
 
 size_t sk_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int64_t d,
                           const sk_kernel_config *cfg) {
   if (!cfg) return 0;
-  size_t need = fast_workspace_bytes(nx, lx, ny, ly, d, *cfg);
-  // float64 path: self levels of X and Y, and the Gram itself
-  if (!fast_supported(lx, lx, d, *cfg)) need = std::max(need, generic_workspace_bytes(nx, lx, lx, *cfg));
-  if (ny > 0) {
-    if (!fast_supported(ly, ly, d, *cfg))
-      need = std::max(need, generic_workspace_bytes(ny, ly, ly, *cfg));
-    if (!fast_supported(lx, ly, d, *cfg))
-      need = std::max(need, generic_workspace_bytes(nx * ny, lx, ly, *cfg));
-  }
+  // the largest need of the calls a Gram makes: self levels of X and of Y
+  // (normalisation) and the Gram itself, each on the path it dispatches to
+  auto use = [&](int64_t n1, int64_t l1, int64_t n2, int64_t l2) -> size_t {
+    const int path = n2 > 0 ? path_of(l1, l2, d, *cfg) : path_of(l1, l1, d, *cfg);
+    if (path == 1) return fast_workspace_bytes(n1, l1, n2, l2, d, *cfg);
+    if (path == 2) return gemm_workspace_bytes(n1, l1, n2, l2, d, *cfg);
+    return n2 > 0 ? generic_workspace_bytes(n1 * n2, l1, l2, *cfg)
+                  : generic_workspace_bytes(n1, l1, l1, *cfg);
+  };
+  size_t need = use(nx, lx, 0, 0);
+  if (ny > 0) need = std::max({need, use(ny, ly, 0, 0), use(nx, lx, ny, ly)});
   return need;
 }
 
@@ -102,6 +104,8 @@ int sk_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
   cudaStream_t st = (cudaStream_t)stream;
   if (fast_supported(l, l, d, *cfg))
     return fast_self_levels(X, n, l, d, *cfg, out, workspace, workspace_bytes, st);
+  if (gemm_supported(l, l, d, *cfg))
+    return gemm_self_levels(X, n, l, d, *cfg, out, workspace, workspace_bytes, st);
   if ((rc = check_generic_limits(*cfg))) return rc;
   return generic_self_levels(X, n, l, d, *cfg, out, workspace, workspace_bytes, st);
 }
@@ -131,6 +135,10 @@ int sk_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny
   cudaStream_t st = (cudaStream_t)stream;
   if (fast_supported(lx, ly, d, *cfg))
     return fast_gram(X, nx, lx, Y, ny, ly, d, symmetric, *cfg, row_begin, row_end, diag_x,
+                     symmetric ? diag_x : diag_y, K, ldk, levels, workspace, workspace_bytes,
+                     st);
+  if (gemm_supported(lx, ly, d, *cfg))
+    return gemm_gram(X, nx, lx, Y, ny, ly, d, symmetric, *cfg, row_begin, row_end, diag_x,
                      symmetric ? diag_x : diag_y, K, ldk, levels, workspace, workspace_bytes,
                      st);
   if ((rc = check_generic_limits(*cfg))) return rc;

@@ -167,4 +167,24 @@ int fast_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
                      const sk_kernel_config &c, double *out, void *ws, size_t ws_bytes,
                      cudaStream_t st);
 
+// GEMM-fed FP32 path (large d): library GEMM of the cell values + systolic DP.
+bool gemm_supported(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c);
+size_t gemm_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int64_t d,
+                            const sk_kernel_config &c);
+int gemm_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
+              int64_t ly, int64_t d, int symmetric, const sk_kernel_config &c,
+              int64_t row_begin, int64_t row_end, const double *diag_x, const double *diag_y,
+              double *K, int64_t ldk, double *levels, void *ws, size_t ws_bytes,
+              cudaStream_t st);
+int gemm_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
+                     const sk_kernel_config &c, double *out, void *ws, size_t ws_bytes,
+                     cudaStream_t st);
+
+// Path selection: 1 fused, 2 GEMM-fed, 0 float64.
+inline int path_of(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
+  if (fast_supported(lx, ly, d, c)) return 1;
+  if (gemm_supported(lx, ly, d, c)) return 2;
+  return 0;
+}
+
 }  // namespace sk

@@ -222,17 +222,11 @@ bool fast_supported(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c
 
 size_t fast_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int64_t d,
                             const sk_kernel_config &c) {
+  // ny == 0: self levels of (nx, lx); otherwise the Gram of X (nx, lx) vs Y (ny, ly)
   using namespace fast;
-  size_t need = 0;
-  const Plan px = plan_for(lx, lx, d, c);
-  if (px.ok) need = std::max(need, roles_bytes(nx, lx, nx, px));  // self levels / K(X)
-  if (ny > 0) {
-    const Plan py = plan_for(ly, ly, d, c);
-    if (py.ok) need = std::max(need, roles_bytes(ny, ly, ny, py));
-    const Plan pg = plan_for(lx, ly, d, c);
-    if (pg.ok) need = std::max(need, roles_bytes(nx, lx, ny, pg));
-  }
-  return need;
+  const Plan pl = ny > 0 ? plan_for(lx, ly, d, c) : plan_for(lx, lx, d, c);
+  if (!pl.ok) return 0;
+  return roles_bytes(nx, lx, ny > 0 ? ny : nx, pl);
 }
 
 int fast_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,

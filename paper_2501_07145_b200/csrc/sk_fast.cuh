@@ -97,6 +97,10 @@ struct Params {
   float *carry;  // [max_ctas * NWARPS][rx + 2 jobs][lx2 steps][nhp]
   int nhp;       // floats per carry entry (2 x NCA chain values, 2 x lastD, kout; padded to 4)
   int max_ctas;  // grid size the carry buffer was sized for
+  // GEMM-fed path (sk_gemm.cu): pair (x, y) row r of the cell matrix is at
+  // S + (x - x_blk0) * s_xstride + y * s_ystride + r * s_ld
+  const float *S;
+  int64_t s_ld, s_xstride, s_ystride, x_blk0;
 };
 
 typedef unsigned long long u64;
@@ -176,6 +180,43 @@ __device__ __forceinline__ void write_pair(const Params &P, int64_t i, int64_t j
   }
 }
 
+// A = D(g) - D(g-1), D = G(r,.) - G(r-1,.) for rows a, b of a row pair.
+// dla/dlb: D of the column left of this lane (lane q-1's last column, or the
+// previous panel's); zero_left: column -1 does not exist (A = 0).
+// Linear kind: both roles hold increments (pack kernels), so the point kernel
+// already is A = <dx_i, dy_j> (kernels.py:281 is bilinear), without the
+// cancellation of differencing the point Gram in FP32.
+template <int C, bool LINEAR>
+__device__ __forceinline__ void double_difference(const float (&ga)[C], const float (&gb)[C],
+                                                  float (&prevG)[C], float &lastDa, float &lastDb,
+                                                  float dla, float dlb, bool zero_left,
+                                                  float (&aa)[C], float (&ab)[C]) {
+  if constexpr (LINEAR) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      aa[c] = ga[c];
+      ab[c] = gb[c];
+    }
+  } else {
+    float dva[C], dvb[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      dva[c] = ga[c] - prevG[c];
+      dvb[c] = gb[c] - ga[c];
+      prevG[c] = gb[c];
+    }
+    aa[0] = zero_left ? 0.f : dva[0] - dla;
+    ab[0] = zero_left ? 0.f : dvb[0] - dlb;
+#pragma unroll
+    for (int c = 1; c < C; ++c) {
+      aa[c] = dva[c] - dva[c - 1];
+      ab[c] = dvb[c] - dvb[c - 1];
+    }
+    lastDa = dva[C - 1];
+    lastDb = dvb[C - 1];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Point stage shared by the lane states: this lane's C y columns in
 // registers, the packed-FFMA2 point kernel of a row pair, and the double
@@ -247,38 +288,56 @@ struct PointStage {
     }
   }
 
-  // A = D(g) - D(g-1), D = G(r,.) - G(r-1,.). dla/dlb: D of the column left
-  // of this lane (lane q-1's last column, or the previous panel's);
-  // zero_left: column -1 does not exist (A = 0).
-  // Linear kind: both roles are packed as increments (pack kernels), so the
-  // point kernel already is A = <dx_i, dy_j> (kernels.py:281 is bilinear),
-  // without the cancellation of differencing the point Gram in FP32.
   __device__ __forceinline__ void increments(float dla, float dlb, bool zero_left, float (&aa)[C],
                                              float (&ab)[C]) {
-    if constexpr (LINEAR) {
+    double_difference<C, LINEAR>(ga, gb, prevG, lastDa, lastDb, dla, dlb, zero_left, aa, ab);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// GEMM-fed stage (large d, sk_gemm.cu): the exponent (rbf, with the n-terms
+// folded into the GEMM's K) or the increment inner product (linear) of every
+// cell was produced by a library GEMM into HBM; a row pair is two rows of
+// that matrix, `ld` floats apart.
+// ---------------------------------------------------------------------------
+template <int C_, bool LINEAR>
+struct GemmStage {
+  static constexpr int C = C_;
+  float prevG[C];
+  float lastDa, lastDb;
+  float ga[C], gb[C];
+  int64_t ld;
+
+  __device__ __forceinline__ void reset_y() {
+#pragma unroll
+    for (int c = 0; c < C; ++c) prevG[c] = 0.f;
+    lastDa = lastDb = 0.f;
+  }
+  __device__ __forceinline__ void point(const float *__restrict__ srow) {
+#pragma unroll
+    for (int c4 = 0; c4 < C / 4; ++c4) {
+      const float4 va = __ldcs(reinterpret_cast<const float4 *>(srow) + c4);  // read once
+      const float4 vb = __ldcs(reinterpret_cast<const float4 *>(srow + ld) + c4);
+      ga[4 * c4 + 0] = va.x;
+      ga[4 * c4 + 1] = va.y;
+      ga[4 * c4 + 2] = va.z;
+      ga[4 * c4 + 3] = va.w;
+      gb[4 * c4 + 0] = vb.x;
+      gb[4 * c4 + 1] = vb.y;
+      gb[4 * c4 + 2] = vb.z;
+      gb[4 * c4 + 3] = vb.w;
+    }
+    if (!LINEAR) {
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        aa[c] = ga[c];
-        ab[c] = gb[c];
+        ga[c] = ex2_approx(fminf(ga[c], 0.f));
+        gb[c] = ex2_approx(fminf(gb[c], 0.f));
       }
-      return;
     }
-    float dva[C], dvb[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      dva[c] = ga[c] - prevG[c];
-      dvb[c] = gb[c] - ga[c];
-      prevG[c] = gb[c];
-    }
-    aa[0] = zero_left ? 0.f : dva[0] - dla;
-    ab[0] = zero_left ? 0.f : dvb[0] - dlb;
-#pragma unroll
-    for (int c = 1; c < C; ++c) {
-      aa[c] = dva[c] - dva[c - 1];
-      ab[c] = dvb[c] - dvb[c - 1];
-    }
-    lastDa = dva[C - 1];
-    lastDb = dvb[C - 1];
+  }
+  __device__ __forceinline__ void increments(float dla, float dlb, bool zero_left, float (&aa)[C],
+                                             float (&ab)[C]) {
+    double_difference<C, LINEAR>(ga, gb, prevG, lastDa, lastDb, dla, dlb, zero_left, aa, ab);
   }
 };
 
@@ -299,10 +358,9 @@ __device__ __forceinline__ void chain_in(const float (&out)[N], float (&in)[N], 
 // ---------------------------------------------------------------------------
 // Order p = 1 lane state (C = 8 columns per lane).
 // ---------------------------------------------------------------------------
-template <int D, int M_, bool LINEAR>
-struct LaneState1 : PointStage<D, 8, LINEAR> {
-  using Base = PointStage<D, 8, LINEAR>;
-  using Base::C;
+template <class Stage, int M_>
+struct LaneState1 : Stage {
+  using Stage::C;
   static constexpr int M = M_;
   static constexpr int NCA = (M >= 2) ? M - 1 : 0;  // column-accumulated levels 1..M-1
   static constexpr int NCR = (NCA > 0) ? NCA : 1;
@@ -423,10 +481,9 @@ struct LaneState1 : PointStage<D, 8, LINEAR> {
 // plus, for S, the cross-lane chain; E_j is a pure row prefix: a running sum
 // along the lane's columns plus a cross-lane chain, exactly like S.
 // ---------------------------------------------------------------------------
-template <int D, int M_, int P, bool LINEAR>
-struct LaneStateG : PointStage<D, 4, LINEAR> {
-  using Base = PointStage<D, 4, LINEAR>;
-  using Base::C;
+template <class Stage, int M_, int P>
+struct LaneStateG : Stage {
+  using Stage::C;
   using Cell = GeoCell<M_, P>;  // generated straight-line cell (sk_geo_cells.cuh)
   static constexpr int M = M_;
   static_assert(P >= 2 && P <= M, "general-order lane state needs 2 <= p <= M");
@@ -677,22 +734,22 @@ template <int D, bool LIN>
 int launch_impl_lin(const Params &P, int M, int order, size_t smem, cudaStream_t st) {
   if (order == 1) {
     switch (M) {
-      case 1: return launch_kernel<LaneState1<D, 1, LIN>>(P, smem, st);
-      case 2: return launch_kernel<LaneState1<D, 2, LIN>>(P, smem, st);
-      case 3: return launch_kernel<LaneState1<D, 3, LIN>>(P, smem, st);
-      case 4: return launch_kernel<LaneState1<D, 4, LIN>>(P, smem, st);
-      case 5: return launch_kernel<LaneState1<D, 5, LIN>>(P, smem, st);
-      case 6: return launch_kernel<LaneState1<D, 6, LIN>>(P, smem, st);
-      case 7: return launch_kernel<LaneState1<D, 7, LIN>>(P, smem, st);
-      case 8: return launch_kernel<LaneState1<D, 8, LIN>>(P, smem, st);
+      case 1: return launch_kernel<LaneState1<PointStage<D, 8, LIN>, 1>>(P, smem, st);
+      case 2: return launch_kernel<LaneState1<PointStage<D, 8, LIN>, 2>>(P, smem, st);
+      case 3: return launch_kernel<LaneState1<PointStage<D, 8, LIN>, 3>>(P, smem, st);
+      case 4: return launch_kernel<LaneState1<PointStage<D, 8, LIN>, 4>>(P, smem, st);
+      case 5: return launch_kernel<LaneState1<PointStage<D, 8, LIN>, 5>>(P, smem, st);
+      case 6: return launch_kernel<LaneState1<PointStage<D, 8, LIN>, 6>>(P, smem, st);
+      case 7: return launch_kernel<LaneState1<PointStage<D, 8, LIN>, 7>>(P, smem, st);
+      case 8: return launch_kernel<LaneState1<PointStage<D, 8, LIN>, 8>>(P, smem, st);
       default: break;
     }
   } else if (order == M) {
     switch (M) {
-      case 2: return launch_kernel<LaneStateG<D, 2, 2, LIN>>(P, smem, st);
-      case 3: return launch_kernel<LaneStateG<D, 3, 3, LIN>>(P, smem, st);
-      case 4: return launch_kernel<LaneStateG<D, 4, 4, LIN>>(P, smem, st);
-      case 5: return launch_kernel<LaneStateG<D, 5, 5, LIN>>(P, smem, st);
+      case 2: return launch_kernel<LaneStateG<PointStage<D, 4, LIN>, 2, 2>>(P, smem, st);
+      case 3: return launch_kernel<LaneStateG<PointStage<D, 4, LIN>, 3, 3>>(P, smem, st);
+      case 4: return launch_kernel<LaneStateG<PointStage<D, 4, LIN>, 4, 4>>(P, smem, st);
+      case 5: return launch_kernel<LaneStateG<PointStage<D, 4, LIN>, 5, 5>>(P, smem, st);
       default: break;
     }
   }

@@ -1,0 +1,490 @@
+// GEMM-fed FP32 path for channel counts the fused kernel cannot hold in
+// registers (d > 16, e.g. BASELINE c4: linear, d = 128).
+//
+// The cell values of a block of pairs are one dense contraction:
+//   rbf:    s(i, j) = <x'_i, y'_j> + n(x'_i) + n(y'_j)   (G = exp2(min(s, 0)))
+//   linear: a(i, j) = <dx_i, dy_j>                         (A directly, kernels.py:281)
+// with the n-terms folded into K as two extra columns ([x', n_x, 1] . [y', 1, n_y]).
+// A library GEMM (cuBLAS, FP32-accurate: BF16x9 FP32 emulation on the tensor
+// cores where the loaded cuBLAS offers it, plain FP32 otherwise) writes it for
+// a block of x sequences against all y into HBM, and `gemm_dp_kernel` streams
+// it through the same systolic lane states as the fused kernel (GemmStage
+// instead of PointStage): lane q of a segment reads its C columns of two rows
+// per step (coalesced 16-lane rows), runs the double difference (rbf) and
+// the level recursion, and writes the finished Gram entries. The DP stage is
+// HBM-bound by design (4 bytes read per cell); the GEMM is tensor/FP32-bound.
+#include <cublas_v2.h>
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+
+#include "sk_fast.cuh"
+
+namespace sk {
+namespace gemm {
+
+using fast::NTHREADS;
+using fast::NWARPS;
+using fast::Params;
+
+// The fused kernel's epoch/panel structure without the shared-memory x ring:
+// every lane addresses its pair's rows in the cell matrix directly.
+template <class LS, bool MULTI>
+__global__ void __launch_bounds__(NTHREADS) gemm_dp_kernel(const Params P) {
+  constexpr int M = LS::M;
+  constexpr int C = LS::C;
+  const int lx2 = P.lx2;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int sw = P.sw;
+  const int q = lane & (sw - 1);
+  const int seg = warp * (32 / sw) + lane / sw;
+  const bool last_lane = (q == sw - 1);
+  const bool first_lane = (q == 0);
+  const int64_t rowpair = 2 * P.s_ld;  // floats between row pairs
+
+  LS st;
+  st.ld = P.s_ld;
+  for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x) {
+    const int64_t ty = tile % P.tiles_y;
+    const int64_t tx = tile / P.tiles_y;
+    const int64_t ybase = ty * P.segs;
+    int64_t x0, njobs;
+    if (P.diag_mode) {
+      x0 = ybase;
+      njobs = min((int64_t)P.segs, P.ny - x0);
+    } else {
+      x0 = P.row_begin + tx * P.rx;
+      njobs = min((int64_t)P.rx, P.row_end - x0);
+      if (P.symmetric && x0 > ybase + P.segs - 1) continue;
+    }
+    const int64_t j = ybase + seg;
+    const bool jvalid = j < P.ny;
+    const int64_t jj = jvalid ? j : P.ny - 1;
+    // row 0 of pair (x, jj) at this lane's first column of panel 0
+    auto pair_base = [&](int64_t x) -> const float * {
+      const int64_t xl = min(max(x, x0), x0 + njobs - 1) - P.x_blk0;
+      return P.S + xl * P.s_xstride + jj * P.s_ystride + (int64_t)q * C;
+    };
+    float *cbuf = MULTI ? P.carry + ((size_t)(blockIdx.x * NWARPS + warp) * (P.rx + 2)) * lx2 * P.nhp
+                        : nullptr;
+    const int npanel = MULTI ? P.npanel : 1;
+    for (int pnl = 0; pnl < npanel; ++pnl) {
+      const int64_t pcol = (int64_t)pnl * 32 * C;
+      st.reset_y();
+      st.reset_panel();
+      const bool head_buf = MULTI && pnl > 0;
+      const bool tail_buf = MULTI && pnl < npanel - 1;
+      const bool last_panel = pnl == npanel - 1;
+      if (MULTI) __syncwarp();  // carries of the previous panel (same warp) are visible
+      constexpr int NHM = LS::NHM;
+      float hcur[NHM], hnext[NHM];
+#pragma unroll
+      for (int k = 0; k < NHM; ++k) hcur[k] = hnext[k] = 0.f;
+      auto load_head = [&](float (&h)[NHM], int64_t job, int rp) {
+        if (head_buf && first_lane) {
+          const float *src = cbuf + ((size_t)job * lx2 + rp) * P.nhp;
+#pragma unroll
+          for (int k = 0; k < NHM; ++k) h[k] = src[k];
+        }
+      };
+      auto store_tail = [&](int64_t job, int rp) {
+        if (tail_buf && last_lane && job >= 0)
+          st.store_carry(cbuf + ((size_t)job * lx2 + rp) * P.nhp);
+      };
+      load_head(hcur, 0, 0);
+      for (int64_t e = 0; e <= njobs; ++e) {
+        const float *cur = pair_base(x0 + e) + pcol;
+        const float *prev = pair_base(e == 0 ? x0 : x0 + e - 1) + pcol;
+        const int steps = (e < njobs) ? lx2 : sw;
+        const int nA = min(sw, steps);
+        for (int s = 0; s < nA; ++s) {
+          if (MULTI) load_head(hnext, s + 1 < steps ? e : e + 1, s + 1 < steps ? s + 1 : 0);
+          const float *xp = (s < q) ? prev + (int64_t)(lx2 - q + s) * rowpair
+                                    : cur + (int64_t)(s - q) * rowpair;
+          st.template step<true, MULTI, true>(xp, sw, first_lane, hcur, head_buf, s == q);
+          if (MULTI) {
+            if (s >= q)
+              store_tail(e, s - q);
+            else
+              store_tail(e - 1, lx2 - q + s);
+          }
+          if (s == q && last_panel && last_lane && e >= 1 && jvalid)
+            fast::write_pair<M>(P, x0 + e - 1, j, st.level_sums(), st.kout);
+          if (MULTI) {
+#pragma unroll
+            for (int k = 0; k < NHM; ++k) hcur[k] = hnext[k];
+          }
+        }
+        const float *xp = cur + (int64_t)(nA - q) * rowpair;
+#pragma unroll 2
+        for (int s = nA; s < steps; ++s) {
+          if (MULTI) load_head(hnext, s + 1 < steps ? e : e + 1, s + 1 < steps ? s + 1 : 0);
+          st.template step<false, MULTI, false>(xp, sw, first_lane, hcur, head_buf, false);
+          if (MULTI) {
+            store_tail(e, s - q);
+#pragma unroll
+            for (int k = 0; k < NHM; ++k) hcur[k] = hnext[k];
+          }
+          xp += rowpair;
+        }
+      }
+    }
+  }
+}
+
+// Dense GEMM operand rows: [n][rows][K] float32.
+//  mode 0 (rbf, x role): [x' (d), n_x, 1, 0...]    mode 1 (rbf, y role): [y', 1, n_y, 0...]
+//  mode 2 (linear, both roles): [dx (d), 0...] with dx_0 = 0 (as pack_x/pack_y incr)
+// Rows beyond L repeat the last point (rbf) / are zero increments (linear).
+__global__ void pack_rows_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
+                                 int64_t rows, int K, double coord_scale, int mode,
+                                 float *__restrict__ out) {
+  const int64_t total = n * rows;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = t / rows, r = t % rows;
+    const double *seq = X + s * L * d;
+    const int64_t pt = min(r, L - 1);
+    float *dst = out + t * K;
+    double nrm = 0.0;
+    for (int k = 0; k < d; ++k) {
+      double v = seq[pt * d + k];
+      if (mode == 2) v = (r >= 1 && r < L) ? v - seq[(pt - 1) * d + k] : 0.0;
+      const float f = (float)(v * coord_scale);
+      dst[k] = f;
+      nrm += (double)f * (double)f;
+    }
+    for (int k = (int)d; k < K; ++k) dst[k] = 0.f;
+    if (mode == 0) {
+      dst[d] = (float)(-0.5 * nrm);
+      dst[d + 1] = 1.f;
+    } else if (mode == 1) {
+      dst[d] = 1.f;
+      dst[d + 1] = (float)(-0.5 * nrm);
+    }
+  }
+}
+
+namespace {
+
+constexpr int RX_MULTI = 8;
+constexpr size_t S_BLOCK_BYTES = size_t(2) << 30;  // cell-matrix block budget
+
+struct Plan {
+  bool ok = false;
+  int C = 8, sw = 0, segs = 0, npanel = 1, nhp = 0, K = 0;
+  bool linear = false;
+};
+
+int next_pow2(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+Plan plan_for(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
+  Plan pl;
+  const int kind = c.static_spec.kind;
+  if (c.precision != SK_PREC_FP32 || !c.difference) return pl;
+  if (kind != SK_RBF && kind != SK_LINEAR) return pl;
+  if (!fast::fast_orders_supported(c.n_levels, c.order)) return pl;
+  if (kind == SK_LINEAR && c.order > 1 && c.normalization != SK_NORM_NONE) return pl;
+  if (d < 1 || lx < 2 || ly < 2) return pl;
+  pl.linear = kind == SK_LINEAR;
+  pl.K = (int)((pl.linear ? d : d + 2) + 3) / 4 * 4;
+  const int C = pl.C = fast::columns_per_lane(c.order);
+  if (ly <= 32 * C) {
+    pl.sw = next_pow2((int)((ly + C - 1) / C));
+  } else {
+    pl.sw = 32;
+    pl.npanel = (int)((ly + 32 * C - 1) / (32 * C));
+    int nch = c.n_levels >= 2 ? c.n_levels - 1 : 0;
+    if (c.order > 1)
+      for (int m = 1; m < c.n_levels; ++m) nch += std::min(m + 1, (int)c.order) - 1;
+    pl.nhp = (2 * nch + 3 + 3) / 4 * 4;
+  }
+  if ((lx + 1) / 2 < pl.sw) return pl;
+  pl.segs = NWARPS * (32 / pl.sw);
+  pl.ok = true;
+  return pl;
+}
+
+size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+int64_t rows_x(int64_t lx) { return 2 * ((lx + 1) / 2); }
+int64_t cols_y(const Plan &pl) { return (int64_t)pl.sw * pl.C * pl.npanel; }
+
+double coord_scale(const sk_kernel_config &c) {
+  if (c.static_spec.kind == SK_LINEAR) return std::sqrt(c.static_spec.scale);
+  return std::sqrt(1.4426950408889634) / c.static_spec.bandwidth;
+}
+
+size_t carry_bytes(int64_t lx, const Plan &pl) {
+  if (pl.npanel <= 1) return 0;
+  return align256((size_t)sm_count() * NWARPS * (RX_MULTI + 2) * ((lx + 1) / 2) * pl.nhp * 4);
+}
+
+// x sequences per GEMM block so that the block's cell matrix fits the budget
+int64_t block_rows(int64_t nx, int64_t lx, int64_t ny, const Plan &pl) {
+  const size_t per_x = (size_t)rows_x(lx) * ny * cols_y(pl) * 4;
+  return std::max<int64_t>(1, std::min<int64_t>(nx, (int64_t)(S_BLOCK_BYTES / std::max<size_t>(per_x, 1))));
+}
+
+size_t gram_bytes(int64_t nx, int64_t lx, int64_t ny, const Plan &pl) {
+  const int64_t bx = block_rows(nx, lx, ny, pl);
+  return align256((size_t)nx * rows_x(lx) * pl.K * 4) + align256((size_t)ny * cols_y(pl) * pl.K * 4) +
+         align256((size_t)bx * rows_x(lx) * ny * cols_y(pl) * 4) + carry_bytes(lx, pl);
+}
+
+size_t self_bytes(int64_t n, int64_t l, const Plan &pl) {
+  return align256((size_t)n * rows_x(l) * pl.K * 4) + align256((size_t)n * cols_y(pl) * pl.K * 4) +
+         align256((size_t)n * rows_x(l) * cols_y(pl) * 4) + carry_bytes(l, pl);
+}
+
+// one cuBLAS handle per (host thread, device)
+cublasHandle_t handle_for_device() {
+  thread_local std::map<int, cublasHandle_t> handles;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto it = handles.find(dev);
+  if (it != handles.end()) return it->second;
+  cublasHandle_t h = nullptr;
+  if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
+  handles[dev] = h;
+  return h;
+}
+
+// FP32-accurate compute type: BF16x9 emulation if this cuBLAS has it, else FP32
+cublasComputeType_t g_compute = CUBLAS_COMPUTE_32F_EMULATED_16BFX9;
+
+// C (m x n, col-major, ldc) = A^T B with A (k x m, lda = k), B (k x n, ldb = k),
+// optionally batched with the given strides.
+int gemm_tn(cudaStream_t st, int64_t m, int64_t n, int64_t k, const float *A, int64_t sa,
+            const float *B, int64_t sb, float *Cm, int64_t ldc, int64_t sc, int64_t batch) {
+  cublasHandle_t h = handle_for_device();
+  if (!h) return fail(SK_ERR_CUDA, "cublasCreate failed");
+  if (cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS) return fail(SK_ERR_CUDA, "cublasSetStream failed");
+  const float one = 1.f, zero = 0.f;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    cublasStatus_t s;
+    if (batch == 1)
+      s = cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)m, (int)n, (int)k, &one, A, CUDA_R_32F,
+                       (int)k, B, CUDA_R_32F, (int)k, &zero, Cm, CUDA_R_32F, (int)ldc, g_compute,
+                       CUBLAS_GEMM_DEFAULT);
+    else
+      s = cublasGemmStridedBatchedEx(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)m, (int)n, (int)k, &one, A,
+                                     CUDA_R_32F, (int)k, sa, B, CUDA_R_32F, (int)k, sb, &zero, Cm,
+                                     CUDA_R_32F, (int)ldc, sc, (int)batch, g_compute,
+                                     CUBLAS_GEMM_DEFAULT);
+    if (s == CUBLAS_STATUS_SUCCESS) return SK_OK;
+    if (g_compute != CUBLAS_COMPUTE_32F &&
+        (s == CUBLAS_STATUS_NOT_SUPPORTED || s == CUBLAS_STATUS_INVALID_VALUE)) {
+      g_compute = CUBLAS_COMPUTE_32F;  // this cuBLAS has no FP32 emulation: plain FP32
+      continue;
+    }
+    return fail(SK_ERR_CUDA, "cublas GEMM failed with status " + std::to_string((int)s));
+  }
+  return fail(SK_ERR_CUDA, "cublas GEMM failed");
+}
+
+unsigned pack_blocks(int64_t total) {
+  return (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 16);
+}
+
+int pack(const double *X, int64_t n, int64_t L, int64_t d, int64_t rows, const Plan &pl,
+         const sk_kernel_config &c, bool xrole, float *out, cudaStream_t st) {
+  if (n <= 0) return SK_OK;
+  const int mode = pl.linear ? 2 : (xrole ? 0 : 1);
+  pack_rows_kernel<<<pack_blocks(n * rows), 256, 0, st>>>(X, n, L, d, rows, pl.K, coord_scale(c),
+                                                          mode, out);
+  SK_CHECK_LAUNCH();
+  return SK_OK;
+}
+
+template <class LS>
+int launch_dp(const Params &P, cudaStream_t st) {
+  using K = void (*)(const Params);
+  const K k = P.npanel > 1 ? gemm_dp_kernel<LS, true> : gemm_dp_kernel<LS, false>;
+  int per_sm = 0;
+  SK_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NTHREADS, 0));
+  if (per_sm < 1) per_sm = 1;
+  int64_t cap = (int64_t)sm_count() * per_sm;
+  if (P.npanel > 1) cap = std::min<int64_t>(cap, P.max_ctas);
+  const int grid = (int)std::min<int64_t>(P.ntiles, cap);
+  if (grid <= 0) return SK_OK;
+  k<<<grid, NTHREADS, 0, st>>>(P);
+  SK_CHECK_LAUNCH();
+  return SK_OK;
+}
+
+template <bool LIN>
+int launch_dp_lin(const Params &P, int M, int order, cudaStream_t st) {
+  using fast::LaneState1;
+  using fast::LaneStateG;
+  using S8 = fast::GemmStage<8, LIN>;
+  using S4 = fast::GemmStage<4, LIN>;
+  if (order == 1) {
+    switch (M) {
+      case 1: return launch_dp<LaneState1<S8, 1>>(P, st);
+      case 2: return launch_dp<LaneState1<S8, 2>>(P, st);
+      case 3: return launch_dp<LaneState1<S8, 3>>(P, st);
+      case 4: return launch_dp<LaneState1<S8, 4>>(P, st);
+      case 5: return launch_dp<LaneState1<S8, 5>>(P, st);
+      case 6: return launch_dp<LaneState1<S8, 6>>(P, st);
+      case 7: return launch_dp<LaneState1<S8, 7>>(P, st);
+      case 8: return launch_dp<LaneState1<S8, 8>>(P, st);
+      default: break;
+    }
+  } else if (order == M) {
+    switch (M) {
+      case 2: return launch_dp<LaneStateG<S4, 2, 2>>(P, st);
+      case 3: return launch_dp<LaneStateG<S4, 3, 3>>(P, st);
+      case 4: return launch_dp<LaneStateG<S4, 4, 4>>(P, st);
+      case 5: return launch_dp<LaneStateG<S4, 5, 5>>(P, st);
+      default: break;
+    }
+  }
+  return fail(SK_ERR_UNSUPPORTED, "gemm path: (n_levels, order) not compiled");
+}
+
+Params base_params(const Plan &pl, int64_t lx, float *carry) {
+  Params P{};
+  P.lx2 = (int)((lx + 1) / 2);
+  P.lyp = (int)cols_y(pl);
+  P.sw = pl.sw;
+  P.segs = pl.segs;
+  P.npanel = pl.npanel;
+  P.nhp = pl.nhp;
+  P.carry = carry;
+  P.max_ctas = sm_count();
+  return P;
+}
+
+}  // namespace
+}  // namespace gemm
+
+bool gemm_supported(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
+  return gemm::plan_for(lx, ly, d, c).ok;
+}
+
+size_t gemm_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int64_t d,
+                            const sk_kernel_config &c) {
+  // ny == 0: self levels of (nx, lx); otherwise the Gram of X (nx, lx) vs Y (ny, ly)
+  using namespace gemm;
+  if (ny <= 0) {
+    const Plan pl = plan_for(lx, lx, d, c);
+    return pl.ok ? self_bytes(nx, lx, pl) : 0;
+  }
+  const Plan pl = plan_for(lx, ly, d, c);
+  return pl.ok ? gram_bytes(nx, lx, ny, pl) : 0;
+}
+
+int gemm_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
+              int64_t ly, int64_t d, int symmetric, const sk_kernel_config &c,
+              int64_t row_begin, int64_t row_end, const double *diag_x, const double *diag_y,
+              double *K, int64_t ldk, double *levels, void *ws, size_t ws_bytes,
+              cudaStream_t st) {
+  using namespace gemm;
+  if (symmetric) {
+    Y = X;
+    ny = nx;
+    ly = lx;
+  }
+  const Plan pl = plan_for(lx, ly, d, c);
+  if (!pl.ok) return fail(SK_ERR_UNSUPPORTED, "gemm path does not cover this configuration");
+  const size_t need = gram_bytes(nx, lx, ny, pl);
+  if (!ws || ws_bytes < need)
+    return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
+  const int64_t rx = rows_x(lx), cy = cols_y(pl), bx = block_rows(nx, lx, ny, pl);
+  float *xg = (float *)ws;
+  float *yg = (float *)((char *)ws + align256((size_t)nx * rx * pl.K * 4));
+  float *sblk = (float *)((char *)yg + align256((size_t)ny * cy * pl.K * 4));
+  float *carry = (float *)((char *)sblk + align256((size_t)bx * rx * ny * cy * 4));
+  int rc = pack(X, nx, lx, d, rx, pl, c, true, xg, st);
+  if (!rc) rc = pack(Y, ny, ly, d, cy, pl, c, false, yg, st);
+  if (rc) return rc;
+  if (row_end <= row_begin || ny <= 0) return SK_OK;
+  Params P = base_params(pl, lx, carry);
+  P.nx = nx;
+  P.ny = ny;
+  P.tiles_y = (ny + pl.segs - 1) / pl.segs;
+  P.symmetric = symmetric;
+  P.norm = c.normalization;
+  P.diag_x = diag_x;
+  P.diag_y = symmetric ? diag_x : diag_y;
+  P.K = K;
+  P.ldk = ldk;
+  P.levels = levels;
+  P.S = sblk;
+  P.s_ld = ny * cy;
+  P.s_xstride = rx * ny * cy;
+  P.s_ystride = cy;
+  const int64_t target = (int64_t)sm_count() * 8;
+  for (int64_t b0 = row_begin; b0 < row_end; b0 += bx) {
+    const int64_t b1 = std::min(row_end, b0 + bx), rows = b1 - b0;
+    // cell matrix of x rows [b0, b1) against all y: (rows*rx) x (ny*cy), row-major
+    rc = gemm_tn(st, ny * cy, rows * rx, pl.K, yg, 0, xg + b0 * rx * pl.K, 0, sblk, ny * cy, 0, 1);
+    if (rc) return rc;
+    P.x_blk0 = b0;
+    P.row_begin = b0;
+    P.row_end = b1;
+    const int rx_cap = pl.npanel > 1 ? RX_MULTI : 64;
+    P.rx = (int)std::max<int64_t>(1, std::min<int64_t>(rx_cap, (rows * P.tiles_y + target - 1) / target));
+    P.ntiles = ((rows + P.rx - 1) / P.rx) * P.tiles_y;
+    // symmetric K(X): the kernel writes rows >= row_begin of the full matrix;
+    // cross: rows relative to the caller's row_begin
+    if (!symmetric) {
+      P.K = K ? K + (b0 - row_begin) * ldk : nullptr;
+      P.levels = levels ? levels + (b0 - row_begin) * ldk * (c.n_levels + 1) : nullptr;
+      P.row_begin = b0;  // write_pair subtracts row_begin
+    }
+    rc = pl.linear ? launch_dp_lin<true>(P, c.n_levels, c.order, st)
+                   : launch_dp_lin<false>(P, c.n_levels, c.order, st);
+    if (rc) return rc;
+  }
+  return SK_OK;
+}
+
+int gemm_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
+                     const sk_kernel_config &c, double *out, void *ws, size_t ws_bytes,
+                     cudaStream_t st) {
+  using namespace gemm;
+  const Plan pl = plan_for(l, l, d, c);
+  if (!pl.ok) return fail(SK_ERR_UNSUPPORTED, "gemm path does not cover this configuration");
+  if (n <= 0) return SK_OK;
+  const size_t need = self_bytes(n, l, pl);
+  if (!ws || ws_bytes < need)
+    return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
+  const int64_t rx = rows_x(l), cy = cols_y(pl);
+  float *xg = (float *)ws;
+  float *yg = (float *)((char *)ws + align256((size_t)n * rx * pl.K * 4));
+  float *sb = (float *)((char *)yg + align256((size_t)n * cy * pl.K * 4));
+  float *carry = (float *)((char *)sb + align256((size_t)n * rx * cy * 4));
+  int rc = pack(X, n, l, d, rx, pl, c, true, xg, st);
+  if (!rc) rc = pack(X, n, l, d, cy, pl, c, false, yg, st);
+  if (rc) return rc;
+  // per-sequence cell matrices (pairs (i, i)): batched GEMM, [n][rx][cy]
+  rc = gemm_tn(st, cy, rx, pl.K, yg, cy * pl.K, xg, rx * pl.K, sb, cy, rx * cy, n);
+  if (rc) return rc;
+  Params P = base_params(pl, l, carry);
+  P.nx = P.ny = n;
+  P.tiles_y = (n + pl.segs - 1) / pl.segs;
+  P.ntiles = P.tiles_y;
+  P.rx = pl.segs;
+  P.row_begin = 0;
+  P.row_end = n;
+  P.diag_mode = 1;
+  P.norm = SK_NORM_NONE;
+  P.self_out = out;
+  // pair (x, y) reads sequence x's own matrix (only x == y is kept)
+  P.S = sb;
+  P.s_ld = cy;
+  P.s_xstride = rx * cy;
+  P.s_ystride = 0;
+  P.x_blk0 = 0;
+  return pl.linear ? launch_dp_lin<true>(P, c.n_levels, c.order, st)
+                   : launch_dp_lin<false>(P, c.n_levels, c.order, st);
+}
+
+}  // namespace sk

@@ -32,7 +32,7 @@ from .sequences import SequenceBatch
 from .utils import ResourceCounters, dp_flops
 
 __all__ = ["sig_kernel_gram", "sig_kernel_dp", "sig_levels_dp", "increment_tensor",
-           "self_levels", "uses_fast_path"]
+           "self_levels", "uses_fast_path", "execution_path"]
 
 ALGORITHMS = ("dp", "pde", "bruteforce")  # kernels.py:53
 
@@ -91,10 +91,20 @@ def _workspace(nbytes: int, dev):
     return torch.empty(int(nbytes), dtype=torch.uint8, device=dev), int(nbytes)
 
 
-def uses_fast_path(lx: int, ly: int, d: int, cfg: KernelConfig, precision: str = "fp32") -> bool:
-    """True if this configuration runs on the fused FP32 sm_100a kernels."""
+_PATHS = {0: "fp64", 1: "fused", 2: "gemm"}
+
+
+def execution_path(lx: int, ly: int, d: int, cfg: KernelConfig, precision: str = "fp32") -> str:
+    """Which sm_100a path runs this configuration: "fused" (the fused FP32 Gram
+    kernel, d <= 16), "gemm" (library GEMM of the cell values + the FP32
+    systolic DP kernel, large d) or "fp64" (the general float64 kernel)."""
     c = _native.config_struct(cfg, precision)
-    return bool(_native.load().sk_fast_path(lx, ly, d, c))
+    return _PATHS[_native.load().sk_fast_path(lx, ly, d, c)]
+
+
+def uses_fast_path(lx: int, ly: int, d: int, cfg: KernelConfig, precision: str = "fp32") -> bool:
+    """True if this configuration runs on an FP32 sm_100a path (fused or GEMM-fed)."""
+    return execution_path(lx, ly, d, cfg, precision) != "fp64"
 
 
 # ---------------------------------------------------------------------------

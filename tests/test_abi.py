@@ -41,7 +41,8 @@ def test_fast_path_selection():
     assert lib.sk_fast_path(50, 50, 3, c3) == 1             # c1 shapes
     lin = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="linear"), n_levels=3))
     assert lib.sk_fast_path(128, 128, 16, lin) == 1
-    assert lib.sk_fast_path(128, 128, 128, lin) == 0        # d > 16: float64 path (for now)
+    assert lib.sk_fast_path(128, 128, 128, lin) == 2        # d > 16: GEMM-fed path (c4)
+    assert lib.sk_fast_path(1000, 1000, 16, lin) == 2       # x ring too large for shared memory
     geo = _native.config_struct(KernelConfig(n_levels=5, order=5))
     assert lib.sk_fast_path(128, 128, 8, geo) == 1          # geometric p = M (c2)
     mid = _native.config_struct(KernelConfig(n_levels=5, order=3))
@@ -55,7 +56,7 @@ def test_fast_path_selection():
     assert lib.sk_fast_path(64, 64, 4, mat) == 0
     assert lib.sk_fast_path(300, 300, 4, c3) == 1           # two 256-column panels
     assert lib.sk_fast_path(2048, 2048, 4, _native.config_struct(KernelConfig(n_levels=8))) == 1  # c5
-    assert lib.sk_fast_path(1000, 1000, 16, c3) == 0        # x ring would exceed shared memory
+    assert lib.sk_fast_path(1000, 1000, 16, c3) == 2        # x ring would exceed shared memory
     assert lib.sk_fast_path(2, 256, 4, c3) == 0             # x shorter than the wavefront
 
 

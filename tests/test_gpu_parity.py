@@ -251,3 +251,50 @@ def test_c2_shapes_fused_vs_fp64():
         K32 = sig_kernel_gram(X, Y, cfg=cfg)
         K64 = sig_kernel_gram(X, Y, cfg=cfg, precision="fp64")
         assert _rel(K32, K64) <= tol, norm
+
+
+# ---------------------------------------------------------------------------
+# GEMM-fed path (d > 16 or long x): library GEMM of the cell values + FP32 DP
+# ---------------------------------------------------------------------------
+
+def test_gemm_path_linear_c4_shapes():
+    """c4 shapes (linear, d=128, M=3, unnormalised) sub-block vs the oracle."""
+    from paper_2501_07145_b200.kernels import execution_path
+    X = gen_brownian(6, 128, 128, SeedStream(1)).data
+    Y = gen_brownian(5, 128, 128, SeedStream(2)).data
+    cfg = KernelConfig(static=StaticKernelSpec(kind="linear"), n_levels=3)
+    assert execution_path(128, 128, 128, cfg) == "gemm"
+    R = O.gram(X, Y, sp=O.static_params("linear"), M=3, p=1)
+    assert _rel(sig_kernel_gram(X, Y, cfg=cfg), R) <= TOL_RAW
+
+
+@pytest.mark.parametrize("kind", ["rbf", "linear"])
+@pytest.mark.parametrize("M,p", [(4, 1), (3, 3)])
+def test_gemm_path_kinds_orders(kind, M, p):
+    from paper_2501_07145_b200.kernels import execution_path
+    X = gen_brownian(7, 70, 24, SeedStream(31)).data
+    Y = gen_brownian(6, 50, 24, SeedStream(32)).data
+    sp = O.static_params(kind)
+    norms = (("none", TOL_RAW),) if (kind == "linear" and p > 1) else \
+        (("none", TOL_RAW), ("levelwise", TOL_NORM))
+    for norm, tol in norms:
+        cfg = KernelConfig(static=StaticKernelSpec(kind=kind), n_levels=M, order=p,
+                           normalization=norm)
+        assert execution_path(70, 50, 24, cfg) == "gemm"
+        R = O.gram(X, Y, sp=sp, M=M, p=p, normalization=norm)
+        assert _scaled_err(sig_kernel_gram(X, Y, cfg=cfg), R) <= tol, (kind, M, p, norm)
+        assert _scaled_err(sig_kernel_gram(Y, X, cfg=cfg), R.T) <= tol, (kind, M, p, norm)
+
+
+def test_gemm_path_multi_panel_symmetric_blocks():
+    from paper_2501_07145_b200.kernels import gram_block
+    X = gen_brownian(9, 300, 20, SeedStream(33)).data
+    cfg = KernelConfig(n_levels=4, normalization="levelwise")
+    K = sig_kernel_gram(X, cfg=cfg)
+    assert np.array_equal(K, K.T) and np.array_equal(np.diag(K), np.ones(9))
+    assert _rel(K, O.gram(X, None, M=4, p=1, normalization="levelwise")) <= TOL_NORM
+    Xt = torch.from_numpy(X).cuda()
+    Yt = torch.from_numpy(gen_brownian(4, 280, 20, SeedStream(34)).data).cuda()
+    full, _ = gram_block(Xt, Yt, cfg)
+    parts = [gram_block(Xt, Yt, cfg, r0, r1)[0] for r0, r1 in ((0, 4), (4, 9))]
+    assert torch.equal(torch.cat(parts), full)
