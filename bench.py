@@ -48,6 +48,37 @@ def flops_per_entry(L, d, M):
     return 2 * L * L * (d + 2 * M)
 
 
+def order_aware_flops_per_entry(L, d, M, p):
+    """Work the recursion actually does per entry at order p (SURVEY.md §8(d) note):
+    2d per cell for the static stage, and per level m the min(m,p)^2 states with
+    their row/column/total sums (about 2 flops per state: one multiply, one
+    accumulate) plus 4 per level for the scans. Equals the north-star model at p = 1."""
+    per_cell = 2 * d + sum(2 * min(m, p) ** 2 + 2 for m in range(1, M + 1)) if p > 1 else 2 * d + 4 * M
+    return L * L * per_cell
+
+
+def path_info(name):
+    """(execution path, kernel label, own kernel launches per sk_gram / sk_self_levels call)."""
+    from paper_2501_07145_b200.kernels import execution_path
+    N, L, d, M, p, kind, norm, sym, _ = CONFIGS[name]
+    path = execution_path(L, L, d, kernel_config(name))
+    D = 4 if d <= 4 else (8 if d <= 8 else 16)
+    if path == "fused":
+        state = (f"LaneState1<PointStage<{D},8>,{M}>" if p == 1
+                 else f"LaneStateG<PointStage<{D},4>,{M},{p}>")
+        return path, f"sk::fast::gram_kernel<{state}> (fused Gram)", 3, 3
+    if path == "gemm":
+        # x blocks of the 2 GiB cell-matrix budget (sk_gemm.cu block_rows); one DP launch each
+        C = 8 if p == 1 else 4
+        sw = 32 if L > 32 * C else 1 << max(0, (-(-L // C) - 1).bit_length())
+        cols = sw * C * max(1, -(-L // (32 * C)))
+        rows = 2 * ((L + 1) // 2)
+        bx = max(1, min(N, (2 << 30) // (rows * N * cols * 4)))
+        return (path, "cuBLAS FP32 GEMM (cell values) + sk::gemm::gemm_dp_kernel (systolic DP)",
+                2 + -(-N // bx), 3)
+    return path, "sk::generic_levels_kernel (float64)", 2, 2
+
+
 def make_inputs(name):
     from paper_2501_07145_b200 import SeedStream, gen_brownian
     N, L, d = CONFIGS[name][:3]
@@ -276,6 +307,12 @@ def run_gpu(args):
         pairs = rows * ny
     F = flops_per_entry(L, d, M)
     achieved = pairs * F / (g_ms / 1e3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath) and world == 1:  # measured for the full-size single-GPU launch
+        t = json.load(open(tpath)).get(name)
+        if t:
+            traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
     props = torch.cuda.get_device_properties(dev)
     clocks = clk.summary()
     sm_max = clocks["sm_max_mhz"] or 1965.0
@@ -312,7 +349,8 @@ def run_gpu(args):
                "d2h_bytes_per_step": N * ny * 8, "ms_per_step": e_ms,
                "api": "SignatureKernel(...)(X, Y) on pinned host float64 -> host float64 K"}
 
-    launches_per_step = (2 if norm != "none" else 0) * (1 if sym else 2) + (2 if sym else 3)
+    path, klabel, per_gram, per_self = path_info(name)
+    launches_per_step = (per_self if norm != "none" else 0) * (1 if sym else 2) + per_gram
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": world,
@@ -324,9 +362,12 @@ def run_gpu(args):
             "config": dict(workload(name), parallelism=f"rows{world}" if world > 1 else "single"),
             "e2e": e2e,
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "kernel": "sk::fast::gram_p1_kernel (fused Gram, per-launch CUDA events)",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/traffic.json)",
+                         "kernel": klabel + ", per sk_gram call, CUDA events on its stream",
+                         "path": path,
                          "flops_per_entry": F, "pairs_per_launch": pairs,
+                         "order_aware_flops_per_entry": order_aware_flops_per_entry(L, d, M, p),
                          "kernel_ms": g_ms,
                          "peak_note": f"nominal FP32: {props.multi_processor_count} SMs x 128 "
                                       f"lanes x 2 x {sm_max:.0f} MHz (no FP32 figure in "
