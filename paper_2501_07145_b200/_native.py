@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libsigkern_b200.so")
+# SK_LIB_OVERRIDE: development A/B timing of alternative builds of the same library
+LIB_PATH = os.environ.get("SK_LIB_OVERRIDE") or os.path.join(_HERE, "_lib", "libsigkern_b200.so")
 
 SK_OK, SK_ERR_INVALID, SK_ERR_CUDA, SK_ERR_WORKSPACE, SK_ERR_UNSUPPORTED = range(5)
 KIND_CODES = {"linear": 0, "polynomial": 1, "rbf": 2, "matern12": 3, "matern32": 4,

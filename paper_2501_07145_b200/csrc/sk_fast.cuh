@@ -139,6 +139,25 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
+// carry entries: whole float4s (the carry buffer is 16-byte aligned per entry)
+template <int N>
+__device__ __forceinline__ void store_f4(float *dst, const float (&v)[N]) {
+#pragma unroll
+  for (int k = 0; k < N / 4; ++k)
+    reinterpret_cast<float4 *>(dst)[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+}
+template <int N>
+__device__ __forceinline__ void load_f4(float (&v)[N], const float *src) {
+#pragma unroll
+  for (int k = 0; k < N / 4; ++k) {
+    const float4 t = reinterpret_cast<const float4 *>(src)[k];
+    v[4 * k] = t.x;
+    v[4 * k + 1] = t.y;
+    v[4 * k + 2] = t.z;
+    v[4 * k + 3] = t.w;
+  }
+}
+
 __device__ __forceinline__ void stage_sequence(float *dst, const float *src, int nfloats) {
   for (int k = threadIdx.x * 4; k < nfloats; k += NTHREADS * 4) cp_async16(dst + k, src + k);
   cp_async_commit();
@@ -365,6 +384,7 @@ struct LaneState1 : Stage {
   static constexpr int NCA = (M >= 2) ? M - 1 : 0;  // column-accumulated levels 1..M-1
   static constexpr int NCR = (NCA > 0) ? NCA : 1;
   static constexpr int NHM = 2 * NCA + 3;  // carry entry: couta, coutb, lastDa, lastDb, kout
+  static constexpr int NHP = (NHM + 3) / 4 * 4;  // padded to whole float4s
 
   float colacc[NCR][C];
   float couta[NCR], coutb[NCR];
@@ -388,14 +408,18 @@ struct LaneState1 : Stage {
   // segment's last lane at its boundary step), and k_M = kout
   __device__ __forceinline__ const float *level_sums() const { return couta; }
   __device__ __forceinline__ void store_carry(float *dst) const {
+    float buf[NHP];
 #pragma unroll
     for (int m = 0; m < NCA; ++m) {
-      dst[m] = couta[m];
-      dst[NCA + m] = coutb[m];
+      buf[m] = couta[m];
+      buf[NCA + m] = coutb[m];
     }
-    dst[2 * NCA] = this->lastDa;
-    dst[2 * NCA + 1] = this->lastDb;
-    dst[2 * NCA + 2] = kout;
+    buf[2 * NCA] = this->lastDa;
+    buf[2 * NCA + 1] = this->lastDb;
+    buf[2 * NCA + 2] = kout;
+#pragma unroll
+    for (int k = NHM; k < NHP; ++k) buf[k] = 0.f;
+    store_f4<NHP>(dst, buf);
   }
 
   // Level recursion of one row (p = 1): R_m = A * S(R_{m-1}); cin = the
@@ -491,6 +515,7 @@ struct LaneStateG : Stage {
   static constexpr int NE = Cell::NE;   // E chains / colE
   static constexpr int NCH = NS + NE;   // chain values per row
   static constexpr int NHM = 2 * NCH + 3;
+  static constexpr int NHP = (NHM + 3) / 4 * 4;
 
   float colS[C][NS];
   float colE[C][NE];
@@ -515,14 +540,18 @@ struct LaneStateG : Stage {
   }
   __device__ __forceinline__ const float *level_sums() const { return cha; }
   __device__ __forceinline__ void store_carry(float *dst) const {
+    float buf[NHP];
 #pragma unroll
     for (int k = 0; k < NCH; ++k) {
-      dst[k] = cha[k];
-      dst[NCH + k] = chb[k];
+      buf[k] = cha[k];
+      buf[NCH + k] = chb[k];
     }
-    dst[2 * NCH] = this->lastDa;
-    dst[2 * NCH + 1] = this->lastDb;
-    dst[2 * NCH + 2] = kout;
+    buf[2 * NCH] = this->lastDa;
+    buf[2 * NCH + 1] = this->lastDb;
+    buf[2 * NCH + 2] = kout;
+#pragma unroll
+    for (int k = NHM; k < NHP; ++k) buf[k] = 0.f;
+    store_f4<NHP>(dst, buf);
   }
 
   // Level recursion of one row. cin/cout: [S prefixes | E prefixes].
@@ -619,16 +648,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) gram_kernel(const Params P) {
       stage_sequence(smem, P.xs + (size_t)x0 * lx2 * XP, slot_floats);
 
       // head inputs, prefetched one step ahead (lane 0 reads job e, row pair s)
-      constexpr int NHM = LS::NHM;
+      constexpr int NHM = LS::NHP;
       float hcur[NHM], hnext[NHM];
 #pragma unroll
       for (int k = 0; k < NHM; ++k) hcur[k] = hnext[k] = 0.f;
+      // every lane loads the entry (one broadcast transaction, no divergence);
+      // only the segment head uses it
       auto load_head = [&](float (&h)[NHM], int64_t job, int rp) {
-        if (head_buf && first_lane) {
-          const float *src = cbuf + ((size_t)job * lx2 + rp) * P.nhp;
-#pragma unroll
-          for (int k = 0; k < NHM; ++k) h[k] = src[k];
-        }
+        if (head_buf) load_f4(h, cbuf + ((size_t)job * lx2 + rp) * P.nhp);
       };
       auto store_tail = [&](int64_t job, int rp) {
         if (tail_buf && last_lane && job >= 0)

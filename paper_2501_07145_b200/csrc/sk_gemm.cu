@@ -78,16 +78,12 @@ __global__ void __launch_bounds__(NTHREADS) gemm_dp_kernel(const Params P) {
       const bool tail_buf = MULTI && pnl < npanel - 1;
       const bool last_panel = pnl == npanel - 1;
       if (MULTI) __syncwarp();  // carries of the previous panel (same warp) are visible
-      constexpr int NHM = LS::NHM;
+      constexpr int NHM = LS::NHP;
       float hcur[NHM], hnext[NHM];
 #pragma unroll
       for (int k = 0; k < NHM; ++k) hcur[k] = hnext[k] = 0.f;
       auto load_head = [&](float (&h)[NHM], int64_t job, int rp) {
-        if (head_buf && first_lane) {
-          const float *src = cbuf + ((size_t)job * lx2 + rp) * P.nhp;
-#pragma unroll
-          for (int k = 0; k < NHM; ++k) h[k] = src[k];
-        }
+        if (head_buf) fast::load_f4(h, cbuf + ((size_t)job * lx2 + rp) * P.nhp);
       };
       auto store_tail = [&](int64_t job, int rp) {
         if (tail_buf && last_lane && job >= 0)
