@@ -1,6 +1,5 @@
 # Builds the in-tree sm_100a library paper_2501_07145_b200/_lib/libsigkern_b200.so.
-# cudart is linked statically so the .so loads (symbol check) without a GPU;
-# cuBLAS (the GEMM-fed large-d path) is linked dynamically.
+# cudart is linked statically so the .so loads (symbol check) without a GPU.
 NVCC      ?= nvcc
 ARCH      ?= -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   ?= -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
@@ -22,7 +21,7 @@ $(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
 
 $(LIB): $(OBJS)
 	@mkdir -p $(OUT_DIR)
-	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS) -Xcompiler -fvisibility=hidden -lcublas
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS) -Xcompiler -fvisibility=hidden
 
 clean:
 	rm -rf build $(LIB)

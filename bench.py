@@ -319,35 +319,44 @@ def run_gpu(args):
     peak = props.multi_processor_count * 128 * 2 * sm_max * 1e6 / 1e12
 
     # end to end through the public API from pinned host buffers
-    e2e = None
-    if world == 1:
-        import torch as _t
-        Xp = _t.from_numpy(Xh).pin_memory()
-        Yp = None if Yh is None else _t.from_numpy(Yh).pin_memory()
-        Kh = _t.empty((N, ny), dtype=_t.float64).pin_memory()
-        static = RBFKernel(1.0) if kind == "rbf" else LinearKernel(1.0)
-        sk = SignatureKernel(n_levels=M, order=p, normalization=norm, static_kernel=static)
+    # end to end through the public API from pinned host buffers: the
+    # SignatureKernel facade on one GPU; on N GPUs every rank uploads X, Y,
+    # runs distributed.sharded_gram (its row block + the NCCL all-gather) and
+    # reads the assembled K back
+    import torch as _t
+    Xp = _t.from_numpy(Xh).pin_memory()
+    Yp = None if Yh is None else _t.from_numpy(Yh).pin_memory()
+    Kh = _t.empty((N, ny), dtype=_t.float64).pin_memory()
+    static = RBFKernel(1.0) if kind == "rbf" else LinearKernel(1.0)
+    sk = SignatureKernel(n_levels=M, order=p, normalization=norm, static_kernel=static)
 
-        def e2e_step():
-            Xd = Xp.to(dev, non_blocking=True)
-            Yd = None if Yp is None else Yp.to(dev, non_blocking=True)
-            Kd = sk(Xd, Yd)
-            Kh.copy_(Kd, non_blocking=True)
-            return Kd
+    def e2e_step():
+        Xd = Xp.to(dev, non_blocking=True)
+        Yd = None if Yp is None else Yp.to(dev, non_blocking=True)
+        Kd = sk(Xd, Yd) if world == 1 else sharded_gram(Xd, Yd, cfg)
+        Kh.copy_(Kd, non_blocking=True)
+        return Kd
 
+    e2e_step()
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.e2e_steps):
         e2e_step()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(args.e2e_steps):
-            e2e_step()
-        b.record()
-        torch.cuda.synchronize()
-        e_ms = a.elapsed_time(b) / args.e2e_steps
-        h2d = Xh.nbytes + (0 if Yh is None else Yh.nbytes)
-        e2e = {"value": entries / (e_ms / 1e3), "unit": "entries/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": N * ny * 8, "ms_per_step": e_ms,
-               "api": "SignatureKernel(...)(X, Y) on pinned host float64 -> host float64 K"}
+    b.record()
+    barrier()
+    e_ms = a.elapsed_time(b) / args.e2e_steps
+    if world > 1:
+        tt = torch.tensor([e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e_ms = float(tt.item())
+    h2d = Xh.nbytes + (0 if Yh is None else Yh.nbytes)
+    e2e = {"value": entries / (e_ms / 1e3), "unit": "entries/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": N * ny * 8, "ms_per_step": e_ms,
+           "api": ("SignatureKernel(...)(X, Y)" if world == 1 else
+                   "distributed.sharded_gram(X, Y, cfg) on every rank")
+                  + " from pinned host float64 to host float64 K",
+           "per_rank_bytes": "h2d/d2h counted per rank" if world > 1 else None}
 
     path, klabel, per_gram, per_self = path_info(name)
     launches_per_step = (per_self if norm != "none" else 0) * (1 if sym else 2) + per_gram

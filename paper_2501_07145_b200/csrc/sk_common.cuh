@@ -180,6 +180,12 @@ int gemm_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
                      const sk_kernel_config &c, double *out, void *ws, size_t ws_bytes,
                      cudaStream_t st);
 
+// tcgen05 3xTF32 GEMM (sk_tcgemm.cu): C[b][n][m] = sum_k A[b][m][k] B[b][n][k]
+// from pre-split hi/lo operands (row-major, K a multiple of 4).
+int tc_gemm_3xtf32(const float *Ahi, const float *Alo, int64_t Mtot, const float *Bhi,
+                   const float *Blo, int64_t Ntot, int K, float *C, int64_t ldc, int64_t batch,
+                   int64_t c_bstride, cudaStream_t st);
+
 // Path selection: 1 fused, 2 GEMM-fed, 0 float64.
 inline int path_of(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   if (fast_supported(lx, ly, d, c)) return 1;

@@ -5,19 +5,16 @@
 //   rbf:    s(i, j) = <x'_i, y'_j> + n(x'_i) + n(y'_j)   (G = exp2(min(s, 0)))
 //   linear: a(i, j) = <dx_i, dy_j>                         (A directly, kernels.py:281)
 // with the n-terms folded into K as two extra columns ([x', n_x, 1] . [y', 1, n_y]).
-// A library GEMM (cuBLAS, FP32-accurate: BF16x9 FP32 emulation on the tensor
-// cores where the loaded cuBLAS offers it, plain FP32 otherwise) writes it for
-// a block of x sequences against all y into HBM, and `gemm_dp_kernel` streams
+// The tcgen05 3xTF32 GEMM (sk_tcgemm.cu: TMA -> tcgen05.mma -> TMEM, FP32
+// accuracy from hi/lo TF32 splits) writes it for a block of x sequences
+// against all y into HBM, and `gemm_dp_kernel` streams
 // it through the same systolic lane states as the fused kernel (GemmStage
 // instead of PointStage): lane q of a segment reads its C columns of two rows
 // per step (coalesced 16-lane rows), runs the double difference (rbf) and
 // the level recursion, and writes the finished Gram entries. The DP stage is
 // HBM-bound by design (4 bytes read per cell); the GEMM is tensor/FP32-bound.
-#include <cublas_v2.h>
-
 #include <algorithm>
 #include <cmath>
-#include <map>
 
 #include "sk_fast.cuh"
 
@@ -130,35 +127,49 @@ __global__ void __launch_bounds__(NTHREADS) gemm_dp_kernel(const Params P) {
   }
 }
 
-// Dense GEMM operand rows: [n][rows][K] float32.
+// Dense GEMM operand rows: [n][rows][K] float32, split for 3xTF32 into
+// hi = rna_tf32(v) and lo = rna_tf32(v - hi) (both written).
 //  mode 0 (rbf, x role): [x' (d), n_x, 1, 0...]    mode 1 (rbf, y role): [y', 1, n_y, 0...]
 //  mode 2 (linear, both roles): [dx (d), 0...] with dx_0 = 0 (as pack_x/pack_y incr)
 // Rows beyond L repeat the last point (rbf) / are zero increments (linear).
+__device__ __forceinline__ float rna_tf32(float v) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+  return __uint_as_float(r);
+}
+// lo is rounded to TF32 too: the tensor core would otherwise truncate it
+// (measured: 4.5x the FP32 SGEMM error, tools/diag_c4_precision.py)
+__device__ __forceinline__ void put_split(float *hi, float *lo, int k, float v) {
+  const float h = rna_tf32(v);
+  hi[k] = h;
+  lo[k] = rna_tf32(v - h);
+}
+
 __global__ void pack_rows_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
                                  int64_t rows, int K, double coord_scale, int mode,
-                                 float *__restrict__ out) {
+                                 float *__restrict__ hi, float *__restrict__ lo) {
   const int64_t total = n * rows;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = t / rows, r = t % rows;
     const double *seq = X + s * L * d;
     const int64_t pt = min(r, L - 1);
-    float *dst = out + t * K;
+    float *dh = hi + t * K, *dl = lo + t * K;
     double nrm = 0.0;
     for (int k = 0; k < d; ++k) {
       double v = seq[pt * d + k];
       if (mode == 2) v = (r >= 1 && r < L) ? v - seq[(pt - 1) * d + k] : 0.0;
       const float f = (float)(v * coord_scale);
-      dst[k] = f;
+      put_split(dh, dl, k, f);
       nrm += (double)f * (double)f;
     }
-    for (int k = (int)d; k < K; ++k) dst[k] = 0.f;
+    for (int k = (int)d; k < K; ++k) dh[k] = dl[k] = 0.f;
     if (mode == 0) {
-      dst[d] = (float)(-0.5 * nrm);
-      dst[d + 1] = 1.f;
+      put_split(dh, dl, (int)d, (float)(-0.5 * nrm));
+      put_split(dh, dl, (int)d + 1, 1.f);
     } else if (mode == 1) {
-      dst[d] = 1.f;
-      dst[d + 1] = (float)(-0.5 * nrm);
+      put_split(dh, dl, (int)d, 1.f);
+      put_split(dh, dl, (int)d + 1, (float)(-0.5 * nrm));
     }
   }
 }
@@ -227,73 +238,43 @@ int64_t block_rows(int64_t nx, int64_t lx, int64_t ny, const Plan &pl) {
   return std::max<int64_t>(1, std::min<int64_t>(nx, (int64_t)(S_BLOCK_BYTES / std::max<size_t>(per_x, 1))));
 }
 
+size_t operand_bytes(int64_t n, int64_t rows, const Plan &pl) {  // hi + lo
+  return 2 * align256((size_t)n * rows * pl.K * 4);
+}
+
 size_t gram_bytes(int64_t nx, int64_t lx, int64_t ny, const Plan &pl) {
   const int64_t bx = block_rows(nx, lx, ny, pl);
-  return align256((size_t)nx * rows_x(lx) * pl.K * 4) + align256((size_t)ny * cols_y(pl) * pl.K * 4) +
+  return operand_bytes(nx, rows_x(lx), pl) + operand_bytes(ny, cols_y(pl), pl) +
          align256((size_t)bx * rows_x(lx) * ny * cols_y(pl) * 4) + carry_bytes(lx, pl);
 }
 
 size_t self_bytes(int64_t n, int64_t l, const Plan &pl) {
-  return align256((size_t)n * rows_x(l) * pl.K * 4) + align256((size_t)n * cols_y(pl) * pl.K * 4) +
+  return operand_bytes(n, rows_x(l), pl) + operand_bytes(n, cols_y(pl), pl) +
          align256((size_t)n * rows_x(l) * cols_y(pl) * 4) + carry_bytes(l, pl);
-}
-
-// one cuBLAS handle per (host thread, device)
-cublasHandle_t handle_for_device() {
-  thread_local std::map<int, cublasHandle_t> handles;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  auto it = handles.find(dev);
-  if (it != handles.end()) return it->second;
-  cublasHandle_t h = nullptr;
-  if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
-  handles[dev] = h;
-  return h;
-}
-
-// FP32-accurate compute type: BF16x9 emulation if this cuBLAS has it, else FP32
-cublasComputeType_t g_compute = CUBLAS_COMPUTE_32F_EMULATED_16BFX9;
-
-// C (m x n, col-major, ldc) = A^T B with A (k x m, lda = k), B (k x n, ldb = k),
-// optionally batched with the given strides.
-int gemm_tn(cudaStream_t st, int64_t m, int64_t n, int64_t k, const float *A, int64_t sa,
-            const float *B, int64_t sb, float *Cm, int64_t ldc, int64_t sc, int64_t batch) {
-  cublasHandle_t h = handle_for_device();
-  if (!h) return fail(SK_ERR_CUDA, "cublasCreate failed");
-  if (cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS) return fail(SK_ERR_CUDA, "cublasSetStream failed");
-  const float one = 1.f, zero = 0.f;
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    cublasStatus_t s;
-    if (batch == 1)
-      s = cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)m, (int)n, (int)k, &one, A, CUDA_R_32F,
-                       (int)k, B, CUDA_R_32F, (int)k, &zero, Cm, CUDA_R_32F, (int)ldc, g_compute,
-                       CUBLAS_GEMM_DEFAULT);
-    else
-      s = cublasGemmStridedBatchedEx(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)m, (int)n, (int)k, &one, A,
-                                     CUDA_R_32F, (int)k, sa, B, CUDA_R_32F, (int)k, sb, &zero, Cm,
-                                     CUDA_R_32F, (int)ldc, sc, (int)batch, g_compute,
-                                     CUBLAS_GEMM_DEFAULT);
-    if (s == CUBLAS_STATUS_SUCCESS) return SK_OK;
-    if (g_compute != CUBLAS_COMPUTE_32F &&
-        (s == CUBLAS_STATUS_NOT_SUPPORTED || s == CUBLAS_STATUS_INVALID_VALUE)) {
-      g_compute = CUBLAS_COMPUTE_32F;  // this cuBLAS has no FP32 emulation: plain FP32
-      continue;
-    }
-    return fail(SK_ERR_CUDA, "cublas GEMM failed with status " + std::to_string((int)s));
-  }
-  return fail(SK_ERR_CUDA, "cublas GEMM failed");
 }
 
 unsigned pack_blocks(int64_t total) {
   return (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 16);
 }
 
+// packed hi/lo operand pair of n sequences x rows (hi at `out`, lo after it)
+struct Operand {
+  float *hi, *lo;
+};
+
+Operand carve(void *&cursor, int64_t n, int64_t rows, const Plan &pl) {
+  const size_t b = align256((size_t)n * rows * pl.K * 4);
+  Operand o{(float *)cursor, (float *)((char *)cursor + b)};
+  cursor = (char *)cursor + 2 * b;
+  return o;
+}
+
 int pack(const double *X, int64_t n, int64_t L, int64_t d, int64_t rows, const Plan &pl,
-         const sk_kernel_config &c, bool xrole, float *out, cudaStream_t st) {
+         const sk_kernel_config &c, bool xrole, Operand out, cudaStream_t st) {
   if (n <= 0) return SK_OK;
   const int mode = pl.linear ? 2 : (xrole ? 0 : 1);
   pack_rows_kernel<<<pack_blocks(n * rows), 256, 0, st>>>(X, n, L, d, rows, pl.K, coord_scale(c),
-                                                          mode, out);
+                                                          mode, out.hi, out.lo);
   SK_CHECK_LAUNCH();
   return SK_OK;
 }
@@ -393,9 +374,10 @@ int gemm_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t 
   if (!ws || ws_bytes < need)
     return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
   const int64_t rx = rows_x(lx), cy = cols_y(pl), bx = block_rows(nx, lx, ny, pl);
-  float *xg = (float *)ws;
-  float *yg = (float *)((char *)ws + align256((size_t)nx * rx * pl.K * 4));
-  float *sblk = (float *)((char *)yg + align256((size_t)ny * cy * pl.K * 4));
+  void *cur = ws;
+  const Operand xg = carve(cur, nx, rx, pl);
+  const Operand yg = carve(cur, ny, cy, pl);
+  float *sblk = (float *)cur;
   float *carry = (float *)((char *)sblk + align256((size_t)bx * rx * ny * cy * 4));
   int rc = pack(X, nx, lx, d, rx, pl, c, true, xg, st);
   if (!rc) rc = pack(Y, ny, ly, d, cy, pl, c, false, yg, st);
@@ -420,7 +402,9 @@ int gemm_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t 
   for (int64_t b0 = row_begin; b0 < row_end; b0 += bx) {
     const int64_t b1 = std::min(row_end, b0 + bx), rows = b1 - b0;
     // cell matrix of x rows [b0, b1) against all y: (rows*rx) x (ny*cy), row-major
-    rc = gemm_tn(st, ny * cy, rows * rx, pl.K, yg, 0, xg + b0 * rx * pl.K, 0, sblk, ny * cy, 0, 1);
+    const int64_t xoff = b0 * rx * pl.K;
+    rc = tc_gemm_3xtf32(yg.hi, yg.lo, ny * cy, xg.hi + xoff, xg.lo + xoff, rows * rx, pl.K, sblk,
+                        ny * cy, 1, 0, st);
     if (rc) return rc;
     P.x_blk0 = b0;
     P.row_begin = b0;
@@ -453,15 +437,16 @@ int gemm_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
   if (!ws || ws_bytes < need)
     return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
   const int64_t rx = rows_x(l), cy = cols_y(pl);
-  float *xg = (float *)ws;
-  float *yg = (float *)((char *)ws + align256((size_t)n * rx * pl.K * 4));
-  float *sb = (float *)((char *)yg + align256((size_t)n * cy * pl.K * 4));
+  void *cur = ws;
+  const Operand xg = carve(cur, n, rx, pl);
+  const Operand yg = carve(cur, n, cy, pl);
+  float *sb = (float *)cur;
   float *carry = (float *)((char *)sb + align256((size_t)n * rx * cy * 4));
   int rc = pack(X, n, l, d, rx, pl, c, true, xg, st);
   if (!rc) rc = pack(X, n, l, d, cy, pl, c, false, yg, st);
   if (rc) return rc;
   // per-sequence cell matrices (pairs (i, i)): batched GEMM, [n][rx][cy]
-  rc = gemm_tn(st, cy, rx, pl.K, yg, cy * pl.K, xg, rx * pl.K, sb, cy, rx * cy, n);
+  rc = tc_gemm_3xtf32(yg.hi, yg.lo, cy, xg.hi, xg.lo, rx, pl.K, sb, cy, n, rx * cy, st);
   if (rc) return rc;
   Params P = base_params(pl, l, carry);
   P.nx = P.ny = n;

@@ -1,0 +1,370 @@
+// FP32-accurate GEMM on the 5th-generation tensor cores (tcgen05, sm_100a):
+// 3xTF32 split products accumulated in TMEM.
+//
+//   C[n][m] = sum_k A[m][k] * B[n][k]     (A: Mtot x K, B: Ntot x K, row-major fp32;
+//                                          C row-major with row stride ldc)
+//
+// Inputs arrive pre-split as hi = rna_tf32(x) and lo = rna_tf32(x - hi) (the
+// pack kernels of sk_gemm.cu; an unrounded lo would be truncated by the tensor
+// core), and every k-step issues three MMAs,
+//   D += A_hi B_hi + A_hi B_lo + A_lo B_hi,
+// which keeps ~22 mantissa bits of each product (measured c4 parity:
+// tests/test_gpu_parity.py). It is the cell-value stage of the GEMM-fed path
+// (the increment inner products <dx_i, dy_j> of BASELINE c4).
+//
+// Accuracy: the tensor core's FP32 accumulation error grows with the number
+// of MMAs chained into one accumulator (measured, tools/diag_c4_precision.py:
+// 48 chained MMAs -> 4.5x the FP32 SGEMM error; 12 -> SGEMM level). So the
+// hi*hi products (16 MMAs for K = 128) and the ~2^-11 smaller corrections
+// hi*lo + lo*hi go to two TMEM accumulators (columns 0-255 and 256-511) that
+// the epilogue adds in FP32.
+//
+// Structure (one CTA per SM, persistent over 128 x 256 output tiles):
+//  * warp 8, one thread: TMA producer. Per stage it loads a 32-wide K slice of
+//    A_hi, A_lo (128 rows) and B_hi, B_lo (256 rows) into 128B-swizzled
+//    K-major shared-memory tiles and signals `full[s]` (expect-tx bytes);
+//  * warp 9, one thread: MMA issuer. Per stage 4 k-steps x 3 MMAs
+//    (M=128, N=256, K=8, kind::tf32); tcgen05.commit frees the stage
+//    (`empty[s]`) and, after the last stage of a tile, publishes the
+//    accumulators (`tmem_full`);
+//  * warps 0-7: epilogue. Warp w reads TMEM lanes 32(w%4).. (= rows m of the
+//    tile), columns 128(w/4)..+127 of both accumulators, 16 at a time, sums
+//    them into registers, releases TMEM (`tmem_empty`, so the next tile's
+//    MMAs start) and then stores: one coalesced 128-byte store per column
+//    (C is written n-major, m contiguous).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "sk_common.cuh"
+
+namespace sk {
+namespace tc {
+
+constexpr int BM = 128;          // tile rows (A side, TMEM lanes)
+constexpr int BN = 256;          // tile columns (B side, TMEM columns)
+constexpr int KC = 32;           // K floats per stage (one 128-byte swizzle atom row)
+constexpr int STAGES = 2;
+constexpr int A_BYTES = BM * KC * 4;  // 16 KB per part
+constexpr int B_BYTES = BN * KC * 4;  // 32 KB per part
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+constexpr int NTHREADS = 320;  // 8 epilogue warps, producer, MMA issuer
+constexpr uint32_t TMEM_COLS = 512;
+
+struct TcParams {
+  int64_t Mtot, Ntot, ldc;  // per batch entry
+  int kchunks;
+  int64_t tiles_m, tiles_n, batch;
+  float *C;
+  int64_t c_bstride;  // floats between batch entries of C
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0,
+                                            int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+// shared-memory matrix descriptor: K-major, 128B swizzle, 8-row groups 1024 B apart
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
+  d |= (uint64_t)1 << 16;                           // leading byte offset (unused for SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;                 // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                           // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                           // layout: SWIZZLE_128B
+  return d;
+}
+// instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = 256
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(IDESC), "r"(acc));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
+                   const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
+                   const TcParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte aligned stage buffers (swizzle atoms), then barriers
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t *full = (uint64_t *)(smem + STAGES * STAGE_BYTES);
+  uint64_t *empty = full + STAGES;
+  uint64_t *tfull = empty + STAGES;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&tfull[0], 1);
+    mbar_init(&tempty[0], 8);  // one arrival per epilogue warp
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 9) {  // TMEM allocation (whole warp), owner of the dealloc
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem_base = *tmem_slot;
+  const int64_t tiles_b = P.tiles_m * P.tiles_n;
+  const int64_t ntiles = tiles_b * P.batch;
+
+  if (warp == 8) {
+    if (lane == 0) {  // TMA producer
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int b = (int)(t / tiles_b), tt = (int)(t % tiles_b);
+        const int m0 = (int)((tt / P.tiles_n) * BM), n0 = (int)((tt % P.tiles_n) * BN);
+        for (int kc = 0; kc < P.kchunks; ++kc) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t *st = smem + s * STAGE_BYTES;
+          mbar_expect_tx(&full[s], STAGE_BYTES);
+          tma_load_3d(st, &mAhi, &full[s], kc * KC, m0, b);
+          tma_load_3d(st + A_BYTES, &mAlo, &full[s], kc * KC, m0, b);
+          tma_load_3d(st + 2 * A_BYTES, &mBhi, &full[s], kc * KC, n0, b);
+          tma_load_3d(st + 2 * A_BYTES + B_BYTES, &mBlo, &full[s], kc * KC, n0, b);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {  // MMA issuer
+      int s = 0;
+      uint32_t ph = 0, aph = 0;
+      const uint32_t acc_main = tmem_base, acc_corr = tmem_base + (uint32_t)BN;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        mbar_wait(&tempty[0], aph ^ 1);  // epilogue has drained the accumulators
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        for (int kc = 0; kc < P.kchunks; ++kc) {
+          mbar_wait(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
+          const uint32_t sahi = sa, salo = sa + A_BYTES, sbhi = sa + 2 * A_BYTES,
+                         sblo = sa + 2 * A_BYTES + B_BYTES;
+#pragma unroll
+          for (int ks = 0; ks < KC / 8; ++ks) {  // k-step of 8 tf32 = 32 bytes into the atom
+            const uint32_t off = ks * 32;
+            const uint64_t dah = sw128_desc(sahi + off), dal = sw128_desc(salo + off);
+            const uint64_t dbh = sw128_desc(sbhi + off), dbl = sw128_desc(sblo + off);
+            const uint32_t acc = (kc == 0 && ks == 0) ? 0u : 1u;
+            mma_tf32(acc_corr, dal, dbh, acc);
+            mma_tf32(acc_corr, dah, dbl, 1u);
+            mma_tf32(acc_main, dah, dbh, acc);
+          }
+          mma_commit(&empty[s]);  // stage s is free once these MMAs retire
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        mma_commit(&tfull[0]);  // both accumulators complete
+        aph ^= 1;
+      }
+    }
+  } else {  // epilogue warps 0-7: TMEM lanes 32*(warp%4).., columns 128*(warp/4)..
+    const int quad = warp & 3, half = warp >> 2;
+    uint32_t aph = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t b = t / tiles_b, tt = t % tiles_b;
+      const int64_t m0 = (tt / P.tiles_n) * BM, n0 = (tt % P.tiles_n) * BN + 128 * half;
+      float *Cb = P.C + b * P.c_bstride;
+      mbar_wait(&tfull[0], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(128 * half);
+      float out[128];
+#pragma unroll
+      for (int c0 = 0; c0 < 128; c0 += 16) {
+        uint32_t v[16], w[16];
+        tmem_ld16(taddr + (uint32_t)c0, v);
+        tmem_ld16(taddr + (uint32_t)(BN + c0), w);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) out[c0 + j] = __uint_as_float(v[j]) + __uint_as_float(w[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[0]);  // TMEM free: the next tile's MMAs may start
+      aph ^= 1;
+      const int64_t m = m0 + quad * 32 + lane;
+      if (m < P.Mtot) {
+#pragma unroll
+        for (int j = 0; j < 128; ++j) {
+          const int64_t n = n0 + j;
+          if (n < P.Ntot) __stcs(Cb + n * P.ldc + m, out[j]);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 9) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// split x into hi = rna_tf32(x) and lo = rna_tf32(x - hi)
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__global__ void split_tf32_kernel(const float *__restrict__ x, int64_t n, float *__restrict__ hi,
+                                  float *__restrict__ lo) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const float v = x[t];
+    const float h = tf32_rna(v);
+    hi[t] = h;
+    lo[t] = tf32_rna(v - h);
+  }
+}
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  });
+  return fn;
+}
+
+// 3-D map over `batch` row-major (rows x K) fp32 matrices, box KC x box_rows x 1,
+// 128B swizzle (rows beyond `rows` and K beyond `K` read as zeros)
+int make_map(CUtensorMap *map, const float *base, int64_t rows, int K, int64_t batch, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)K * 4, (cuuint64_t)rows * K * 4};
+  cuuint32_t box[3] = {(cuuint32_t)KC, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return SK_OK;
+}
+
+}  // namespace
+}  // namespace tc
+
+int tf32_split(const float *x, int64_t n, float *hi, float *lo, cudaStream_t st) {
+  if (n <= 0) return SK_OK;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 16);
+  tc::split_tf32_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, n, hi, lo);
+  SK_CHECK_LAUNCH();
+  return SK_OK;
+}
+
+int tc_gemm_3xtf32(const float *Ahi, const float *Alo, int64_t Mtot, const float *Bhi,
+                   const float *Blo, int64_t Ntot, int K, float *C, int64_t ldc, int64_t batch,
+                   int64_t c_bstride, cudaStream_t st) {
+  using namespace tc;
+  if (Mtot <= 0 || Ntot <= 0 || batch <= 0) return SK_OK;
+  if (K % 4) return fail(SK_ERR_INVALID, "tc_gemm: K must be a multiple of 4");
+  CUtensorMap mAhi, mAlo, mBhi, mBlo;
+  int rc;
+  if ((rc = make_map(&mAhi, Ahi, Mtot, K, batch, BM)) || (rc = make_map(&mAlo, Alo, Mtot, K, batch, BM)) ||
+      (rc = make_map(&mBhi, Bhi, Ntot, K, batch, BN)) || (rc = make_map(&mBlo, Blo, Ntot, K, batch, BN)))
+    return rc;
+  TcParams P;
+  P.Mtot = Mtot;
+  P.Ntot = Ntot;
+  P.ldc = ldc;
+  P.kchunks = (K + KC - 1) / KC;
+  P.tiles_m = (Mtot + BM - 1) / BM;
+  P.tiles_n = (Ntot + BN - 1) / BN;
+  P.batch = batch;
+  P.c_bstride = c_bstride;
+  P.C = C;
+  const size_t smem = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+  SK_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+  const int grid = (int)std::min<int64_t>(P.tiles_m * P.tiles_n * batch, sm_count());
+  tc_gemm_kernel<<<grid, NTHREADS, smem, st>>>(mAhi, mAlo, mBhi, mBlo, P);
+  SK_CHECK_LAUNCH();
+  return SK_OK;
+}
+
+}  // namespace sk
+
+// Development entry (tests/test_gpu_parity.py::test_tc_gemm_*): C = A B^T with
+// fp32 inputs split here into hi/lo. Not part of the public ABI header.
+extern "C" __attribute__((visibility("default"))) int sk_dev_tc_gemm(
+    const float *A, int64_t M, const float *B, int64_t N, int32_t K, float *C, int64_t ldc,
+    float *scratch, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  float *ahi = scratch, *alo = ahi + M * K, *bhi = alo + M * K, *blo = bhi + N * K;
+  int rc = sk::tf32_split(A, M * K, ahi, alo, st);
+  if (!rc) rc = sk::tf32_split(B, N * K, bhi, blo, st);
+  if (!rc) rc = sk::tc_gemm_3xtf32(ahi, alo, M, bhi, blo, N, K, C, ldc, 1, 0, st);
+  return rc;
+}

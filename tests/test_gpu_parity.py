@@ -298,3 +298,35 @@ def test_gemm_path_multi_panel_symmetric_blocks():
     full, _ = gram_block(Xt, Yt, cfg)
     parts = [gram_block(Xt, Yt, cfg, r0, r1)[0] for r0, r1 in ((0, 4), (4, 9))]
     assert torch.equal(torch.cat(parts), full)
+
+
+# ---------------------------------------------------------------------------
+# tcgen05 3xTF32 GEMM (cell-value stage of the GEMM-fed path)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 32), (300, 520, 132), (1000, 77, 128)])
+def test_tc_gemm_3xtf32_matches_fp64(M, N, K):
+    import ctypes
+    from paper_2501_07145_b200 import _native
+    lib = _native.load()
+    g = torch.Generator(device="cpu").manual_seed(M + N + K)
+    A = torch.randn(M, K, generator=g, dtype=torch.float64)
+    B = torch.randn(N, K, generator=g, dtype=torch.float64)
+    A32, B32 = A.float().cuda(), B.float().cuda()
+    ldc = M + 3
+    C = torch.full((N, ldc), float("nan"), dtype=torch.float32, device="cuda")
+    scratch = torch.empty(2 * (M + N) * K, dtype=torch.float32, device="cuda")
+    fn = lib.sk_dev_tc_gemm
+    fn.restype = ctypes.c_int
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                   ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+    rc = fn(A32.data_ptr(), M, B32.data_ptr(), N, K, C.data_ptr(), ldc, scratch.data_ptr(),
+            torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, lib.sk_last_error()
+    torch.cuda.synchronize()
+    ref = (B32.double() @ A32.double().T).cpu()  # exact products of the fp32 inputs
+    got = C[:, :M].double().cpu()
+    scale = (B32.double().abs() @ A32.double().abs().T).cpu()
+    err = float(((got - ref).abs() / scale).max())
+    assert err < 1e-6, err  # 3xTF32 ~ FP32 accuracy (1xTF32 would be ~1e-3)
+    assert torch.isnan(C[:, M:]).all()  # nothing written beyond the M columns
