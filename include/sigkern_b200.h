@@ -163,6 +163,15 @@ SK_API int sk_increment_tensor(const double *X, int64_t nx, int64_t lx,
                         int32_t paired, const sk_static_spec *spec, int32_t difference,
                         double *out, void *stream);
 
+/*
+ * Pairwise Euclidean distances of n points (float64, (n, d) row-major), upper
+ * triangle i < j row by row: out has n*(n-1)/2 entries. Same formula as the
+ * reference's _pairwise_sqdist + sqrt (static/kernels.py:108-114, 183-184):
+ * sqrt(max(|x_i|^2 + |x_j|^2 - 2<x_i, x_j>, 0)). Used by median_heuristic
+ * (static/kernels.py:165-187) to derive an RBF bandwidth.
+ */
+SK_API int sk_pairwise_dist(const double *X, int64_t n, int64_t d, double *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

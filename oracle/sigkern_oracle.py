@@ -116,6 +116,22 @@ def point_gram(sp, X, Y):
     return _static_from_sqdist(kind, sp, sq)
 
 
+def median_heuristic(X, max_pairs=1_000_000):
+    """Median pairwise distance over a deterministic subsample (static/kernels.py:165-187)."""
+    X = np.atleast_2d(np.asarray(X, dtype=np.float64))
+    n = X.shape[0]
+    if n < 2:
+        raise ValueError(f"median_heuristic needs at least 2 vectors, got {n}")
+    if n * (n - 1) // 2 > max_pairs:
+        m = max(2, min(n, int((1.0 + math.sqrt(1.0 + 8.0 * max_pairs)) / 2.0)))
+        X = X[np.unique((np.arange(m, dtype=np.int64) * n) // m)]
+        n = X.shape[0]
+    xx = np.einsum("ij,ij->i", X, X)
+    sq = np.maximum(xx[:, None] + xx[None, :] - 2.0 * (X @ X.T), 0.0)  # static/kernels.py:108-114
+    med = float(np.median(np.sqrt(sq[np.triu_indices(n, k=1)])))
+    return med if med > 0.0 else 1.0
+
+
 def increments(sp, X, Y, difference=True):
     """Double-differenced point Gram, (..., L1-1, L2-1) (kernels.py:263-281)."""
     X = np.asarray(X, dtype=np.float64)

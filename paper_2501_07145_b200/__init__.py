@@ -12,6 +12,7 @@ from .facade import (LinearKernel, Matern12Kernel, Matern32Kernel, Matern52Kerne
 from .kernels import (increment_tensor, self_levels, sig_kernel_dp, sig_kernel_gram,
                       sig_levels_dp, uses_fast_path)
 from .sequences import SeedStream, SequenceBatch, gen_brownian
+from .static_kernels import median_heuristic
 from .utils import ResourceCounters
 
 __version__ = "0.1.0"
@@ -22,6 +23,6 @@ __all__ = [
     "StaticKernel", "LinearKernel", "PolynomialKernel", "RBFKernel", "Matern12Kernel",
     "Matern32Kernel", "Matern52Kernel", "RationalQuadraticKernel", "SignatureKernel",
     "increment_tensor", "self_levels", "sig_kernel_dp", "sig_kernel_gram", "sig_levels_dp",
-    "uses_fast_path", "SeedStream", "SequenceBatch", "gen_brownian", "ResourceCounters",
+    "uses_fast_path", "median_heuristic", "SeedStream", "SequenceBatch", "gen_brownian", "ResourceCounters",
     "__version__",
 ]

@@ -182,4 +182,11 @@ int sk_increment_tensor(const double *X, int64_t nx, int64_t lx, const double *Y
                           (cudaStream_t)stream);
 }
 
+int sk_pairwise_dist(const double *X, int64_t n, int64_t d, double *out, void *stream) {
+  clear_error();
+  if (n < 0 || d < 1) return fail(SK_ERR_INVALID, "expected (n, d) points with d >= 1");
+  if (n > 1 && (!X || !out)) return fail(SK_ERR_INVALID, "NULL pointer");
+  return pairwise_dist(X, n, d, out, (cudaStream_t)stream);
+}
+
 }  // extern "C"

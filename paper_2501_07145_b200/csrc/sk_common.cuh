@@ -186,6 +186,9 @@ int tc_gemm_3xtf32(const float *Ahi, const float *Alo, int64_t Mtot, const float
                    const float *Blo, int64_t Ntot, int K, float *C, int64_t ldc, int64_t batch,
                    int64_t c_bstride, cudaStream_t st);
 
+// Upper-triangle pairwise distances (median_heuristic), float64.
+int pairwise_dist(const double *X, int64_t n, int64_t d, double *out, cudaStream_t st);
+
 // Path selection: 1 fused, 2 GEMM-fed, 0 float64.
 inline int path_of(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   if (fast_supported(lx, ly, d, c)) return 1;

@@ -386,4 +386,36 @@ int increment_tensor(const double *X, int64_t nx, int64_t lx, const double *Y, i
   return SK_OK;
 }
 
+// Upper-triangle pairwise distances for median_heuristic (static/kernels.py:165-187).
+__global__ void pairwise_dist_kernel(const double *__restrict__ X, int64_t n, int64_t d,
+                                     double *__restrict__ out) {
+  const int64_t npairs = n * (n - 1) / 2;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < npairs;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    // row i holds n-1-i pairs starting at off(i) = i*(2n-i-1)/2
+    int64_t i = (int64_t)((2.0 * n - 1.0 - sqrt((2.0 * n - 1.0) * (2.0 * n - 1.0) - 8.0 * t)) / 2.0);
+    while (i > 0 && i * (2 * n - i - 1) / 2 > t) --i;
+    while ((i + 1) * (2 * n - i - 2) / 2 <= t) ++i;
+    const int64_t j = t - i * (2 * n - i - 1) / 2 + i + 1;
+    const double *x = X + i * d, *y = X + j * d;
+    double xx = 0.0, yy = 0.0, xy = 0.0;
+    for (int64_t k = 0; k < d; ++k) {
+      xx = fma(x[k], x[k], xx);
+      yy = fma(y[k], y[k], yy);
+      xy = fma(x[k], y[k], xy);
+    }
+    double sq = xx + yy - 2.0 * xy;
+    out[t] = sqrt(sq > 0.0 ? sq : 0.0);
+  }
+}
+
+int pairwise_dist(const double *X, int64_t n, int64_t d, double *out, cudaStream_t st) {
+  const int64_t npairs = n * (n - 1) / 2;
+  if (npairs <= 0) return SK_OK;
+  const int64_t blocks = std::min<int64_t>((npairs + 255) / 256, (int64_t)sm_count() * 32);
+  pairwise_dist_kernel<<<(unsigned)blocks, 256, 0, st>>>(X, n, d, out);
+  SK_CHECK_LAUNCH();
+  return SK_OK;
+}
+
 }  // namespace sk

@@ -330,3 +330,19 @@ def test_tc_gemm_3xtf32_matches_fp64(M, N, K):
     err = float(((got - ref).abs() / scale).max())
     assert err < 1e-6, err  # 3xTF32 ~ FP32 accuracy (1xTF32 would be ~1e-3)
     assert torch.isnan(C[:, M:]).all()  # nothing written beyond the M columns
+
+
+def test_median_heuristic_golden():
+    """median_heuristic (static/kernels.py:165-187) vs the reference's own values."""
+    import os
+    from paper_2501_07145_b200 import median_heuristic
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "median.npz"))
+    names = sorted({k.split("__")[0] for k in z.files})
+    for name in names:
+        got = median_heuristic(z[f"{name}__X"], max_pairs=int(z[f"{name}__max_pairs"]))
+        assert got == pytest.approx(float(z[f"{name}__median"]), rel=1e-12), name
+    assert median_heuristic(np.zeros((4, 2))) == 1.0
+    with pytest.raises(ValueError, match="at least 2"):
+        median_heuristic(np.zeros((1, 2)))
+    with pytest.raises(ValueError, match="max_pairs"):
+        median_heuristic(np.zeros((3, 2)), max_pairs=0)

@@ -76,3 +76,12 @@ def test_hand_values():
     assert O.levels_dp(A, 2, 1)[2] == 0.0
     assert O.levels_dp(A, 2, 2)[2] == pytest.approx(9.0)
     assert O.levels_bruteforce(A, 2, 2)[2] == pytest.approx(9.0)
+
+
+def test_oracle_median_heuristic_golden():
+    """The oracle's median_heuristic restatement reproduces the reference's values."""
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "median.npz"))
+    for name in sorted({k.split("__")[0] for k in z.files}):
+        got = O.median_heuristic(z[f"{name}__X"], max_pairs=int(z[f"{name}__max_pairs"]))
+        assert got == float(z[f"{name}__median"]), name  # same numpy ops: bitwise
