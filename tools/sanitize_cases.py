@@ -1,0 +1,31 @@
+"""Small cases of every kernel path for compute-sanitizer runs (tools/gpu_sanitize.sh)."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2501_07145_b200 import (KernelConfig, SeedStream, StaticKernelSpec, gen_brownian,  # noqa: E402
+                                   median_heuristic, sig_kernel_gram, sig_levels_dp)
+from paper_2501_07145_b200.kernels import execution_path  # noqa: E402
+
+X = gen_brownian(9, 40, 3, SeedStream(1)).data
+Y = gen_brownian(7, 40, 3, SeedStream(2)).data
+cases = [
+    ("fused p1 rbf levelwise", X, Y, KernelConfig(n_levels=5, normalization="levelwise")),
+    ("fused p1 symmetric", X, None, KernelConfig(n_levels=4, normalization="global")),
+    ("fused geometric", X, Y, KernelConfig(n_levels=4, order=4)),
+    ("fused multi-panel", gen_brownian(5, 300, 2, SeedStream(3)).data,
+     gen_brownian(4, 300, 2, SeedStream(4)).data, KernelConfig(n_levels=3, normalization="levelwise")),
+    ("gemm linear d=20", gen_brownian(5, 40, 20, SeedStream(5)).data,
+     gen_brownian(4, 40, 20, SeedStream(6)).data, KernelConfig(static=StaticKernelSpec(kind="linear"), n_levels=3)),
+    ("gemm rbf d=20 levelwise", gen_brownian(5, 40, 20, SeedStream(5)).data,
+     gen_brownian(4, 40, 20, SeedStream(6)).data, KernelConfig(n_levels=3, normalization="levelwise")),
+    ("fp64 generic", X, Y, KernelConfig(n_levels=3, order=2)),
+]
+for name, A, B, cfg in cases:
+    K = sig_kernel_gram(A, B, cfg=cfg)
+    L = A.shape[1]
+    print(f"{name:28s} path={execution_path(L, L, A.shape[2], cfg):6s} finite={bool(np.isfinite(K).all())}")
+print("levels_dp", sig_levels_dp(np.random.default_rng(0).standard_normal((3, 6, 5)), 3, order=2).shape)
+print("median", median_heuristic(X.reshape(-1, 3)))
