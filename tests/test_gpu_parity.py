@@ -12,7 +12,8 @@ import torch
 from conftest import oracle_static, pkg_config
 from oracle import sigkern_oracle as O
 from paper_2501_07145_b200 import (KernelConfig, SeedStream, StaticKernelSpec, gen_brownian,
-                                   increment_tensor, sig_kernel_gram, sig_levels_dp,
+                                   increment_tensor, sig_kernel_dp, sig_kernel_gram,
+                                   sig_levels_dp,
                                    uses_fast_path)
 
 pytestmark = pytest.mark.gpu
@@ -346,3 +347,74 @@ def test_median_heuristic_golden():
         median_heuristic(np.zeros((1, 2)))
     with pytest.raises(ValueError, match="max_pairs"):
         median_heuristic(np.zeros((3, 2)), max_pairs=0)
+
+
+# ---------------------------------------------------------------------------
+# the reference's own known-answer tests, re-pointed at the device path
+# ---------------------------------------------------------------------------
+
+LIN = StaticKernelSpec(kind="linear")
+
+
+def test_criterion_01_device_dp_matches_bruteforce():
+    """test_acceptance.py:61-87: 200 random instances, L <= 5, d <= 3, M <= 3,
+    p in {1, 2}; float64 path at 1e-10, FP32 paths at the north-star 1e-4."""
+    rng = np.random.default_rng(20240601)
+    worst64 = worst32 = 0.0
+    for _ in range(200):
+        L1, L2 = rng.integers(2, 6, size=2)
+        d = int(rng.integers(1, 4))
+        M = int(rng.integers(0, 4))
+        p = int(rng.integers(1, 3))
+        bw = float(rng.uniform(0.5, 2.0))
+        static = LIN if rng.integers(2) == 0 else StaticKernelSpec(kind="rbf", bandwidth=bw)
+        cfg = KernelConfig(static=static, n_levels=M, order=p)
+        x = rng.standard_normal((L1, d))
+        y = rng.standard_normal((L2, d))
+        sp = O.static_params(static.kind, bandwidth=static.bandwidth)
+        bf = O.levels_bruteforce(O.increments(sp, x, y), M, cfg.effective_order)
+        for prec in ("fp64", "fp32"):
+            dp = np.asarray(sig_kernel_dp(x, y, cfg, precision=prec).values)
+            rel = np.abs(dp - bf) / np.maximum(np.abs(bf), 1e-30)
+            rel[(dp == 0.0) & (bf == 0.0)] = 0.0
+            # FP32: judge near-cancelling levels against the level-1 scale
+            sc = np.maximum(np.abs(bf), 1e-3 * max(1.0, float(np.abs(bf).max())))
+            if prec == "fp64":
+                worst64 = max(worst64, float(rel.max()))
+            else:
+                worst32 = max(worst32, float((np.abs(dp - bf) / sc).max()))
+    assert worst64 <= 1e-10, worst64
+    assert worst32 <= TOL_RAW, worst32
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_criterion_02_hand_values(prec):
+    """test_acceptance.py:90-100: linear, x increments (1, 2), y increment (2):
+    k_1 = 6; k_2 = 0 at p = 1, 9 at p = 2."""
+    x = np.array([[0.0], [1.0], [3.0]])
+    y = np.array([[0.0], [2.0]])
+    lv1 = sig_kernel_dp(x, y, KernelConfig(static=LIN, n_levels=2, order=1), precision=prec)
+    lv2 = sig_kernel_dp(x, y, KernelConfig(static=LIN, n_levels=2, order=2), precision=prec)
+    assert abs(lv1[1] - 6.0) <= 1e-12 and lv1[2] == 0.0 and abs(lv2[2] - 9.0) <= 1e-12
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_constant_sequences_give_unit_level_zero(prec):
+    """test_kernels.py:67-72: constant sequences -> (1, 0, ..., 0) exactly."""
+    x = np.ones((4, 2)) * 0.3
+    y = np.ones((3, 2)) * -1.0
+    for cfg in (KernelConfig(static=LIN, n_levels=4, order=2), KernelConfig(n_levels=4),
+                KernelConfig(n_levels=4, order=4)):
+        assert np.array_equal(np.asarray(sig_kernel_dp(x, y, cfg, precision=prec).values),
+                              [1.0, 0, 0, 0, 0])
+
+
+def test_normalised_gram_is_psd_on_fused_paths():
+    """test_kernels.py:428-433: normalised K(X) is positive semi-definite."""
+    X = gen_brownian(30, 40, 3, SeedStream(41)).data
+    for cfg in (KernelConfig(n_levels=5, normalization="levelwise"),
+                KernelConfig(n_levels=4, order=4, normalization="levelwise"),
+                KernelConfig(n_levels=3, normalization="global")):
+        assert uses_fast_path(40, 40, 3, cfg)
+        K = sig_kernel_gram(X, cfg=cfg)
+        assert np.linalg.eigvalsh(K).min() >= -1e-6

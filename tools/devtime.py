@@ -16,6 +16,11 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 prec = sys.argv[3] if len(sys.argv) > 3 else "fp32"
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
+# ad-hoc shapes: name "L<len>d<dim>M<levels>", e.g. L256d4M8 (rbf, order 1, unnormalised)
+if name not in bench.CONFIGS:
+    import re
+    L_, d_, M_ = (int(v) for v in re.match(r"L(\d+)d(\d+)M(\d+)", name).groups())
+    bench.CONFIGS[name] = (n, L_, d_, M_, 1, "rbf", "none", False, 2)
 N, L, d, M, p, kind, norm, sym, _ = bench.CONFIGS[name]
 cfg = bench.kernel_config(name)
 rng = np.random.default_rng(0)
