@@ -172,6 +172,23 @@ SK_API int sk_increment_tensor(const double *X, int64_t nx, int64_t lx,
  */
 SK_API int sk_pairwise_dist(const double *X, int64_t n, int64_t d, double *out, void *stream);
 
+/*
+ * Untruncated signature kernel by the Goursat-PDE solve (algorithm="pde",
+ * kernels.py:334-507): float64, one row-streamed pair per thread.
+ *  K: like sk_gram (cross: rows [row_begin,row_end) at K[(i-row_begin)*ldk+j];
+ *  symmetric: full matrix, upper triangle evaluated and mirrored).
+ *  sk_pde_self: k(x_i, x_i) for global normalisation, out is (n,).
+ *  With difference=1 every sequence needs L >= 2 (one increment).
+ */
+SK_API size_t sk_pde_workspace_bytes(int64_t npairs, int64_t ly, int32_t difference);
+SK_API int sk_pde_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
+                int64_t ly, int64_t d, int32_t symmetric, const sk_static_spec *spec,
+                int32_t difference, int64_t row_begin, int64_t row_end, double *K, int64_t ldk,
+                void *workspace, size_t workspace_bytes, void *stream);
+SK_API int sk_pde_self(const double *X, int64_t n, int64_t l, int64_t d,
+                const sk_static_spec *spec, int32_t difference, double *out,
+                void *workspace, size_t workspace_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -116,6 +116,38 @@ def point_gram(sp, X, Y):
     return _static_from_sqdist(kind, sp, sq)
 
 
+def pde_kernel(sp, x, y, difference=True):
+    """Goursat-PDE value of one pair (kernels.py:334-402), row-streamed restatement:
+    K(0,.) = K(.,0) = 1; K(k,l) = both - K(k-1,l-1) + 0.5*C*both, both = K(k,l-1) + K(k-1,l),
+    C the double-differenced (or raw, difference=False) point kernel of cell (k-1, l-1)."""
+    x = np.asarray(x, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    C = increments(sp, x, y, difference)
+    if difference and (x.shape[0] < 2 or y.shape[0] < 2):
+        raise ValueError("pde kernel needs at least one increment per sequence")
+    T1, T2 = C.shape
+    prev = np.ones(T2 + 1)
+    for k in range(1, T1 + 1):
+        cur = np.ones(T2 + 1)
+        for l in range(1, T2 + 1):
+            both = cur[l - 1] + prev[l]
+            cur[l] = both - prev[l - 1] + 0.5 * C[k - 1, l - 1] * both
+        prev = cur
+    return float(prev[T2])
+
+
+def pde_gram(X, Y=None, sp=None, difference=True, normalization="none"):
+    """Gram of pde_kernel values (kernels.py:476-507, 559-571); small inputs only."""
+    sp = sp or static_params("rbf")
+    Yv = X if Y is None else Y
+    K = np.array([[pde_kernel(sp, a, b, difference) for b in Yv] for a in X])
+    if normalization == "global":
+        sx = np.array([pde_kernel(sp, a, a, difference) for a in X])
+        sy = sx if Y is None else np.array([pde_kernel(sp, b, b, difference) for b in Yv])
+        K = K / np.sqrt(sx[:, None] * sy[None, :])
+    return K
+
+
 def median_heuristic(X, max_pairs=1_000_000):
     """Median pairwise distance over a deterministic subsample (static/kernels.py:165-187)."""
     X = np.atleast_2d(np.asarray(X, dtype=np.float64))

@@ -10,7 +10,7 @@ from .facade import (LinearKernel, Matern12Kernel, Matern32Kernel, Matern52Kerne
                      PolynomialKernel, RationalQuadraticKernel, RBFKernel, SignatureKernel,
                      StaticKernel)
 from .kernels import (increment_tensor, self_levels, sig_kernel_dp, sig_kernel_gram,
-                      sig_levels_dp, uses_fast_path)
+                      sig_levels_dp, sig_pde_kernel, uses_fast_path)
 from .sequences import SeedStream, SequenceBatch, gen_brownian
 from .static_kernels import median_heuristic
 from .utils import ResourceCounters
@@ -22,7 +22,7 @@ __all__ = [
     "ConfigError", "NativeError", "NumericError", "SigkernError",
     "StaticKernel", "LinearKernel", "PolynomialKernel", "RBFKernel", "Matern12Kernel",
     "Matern32Kernel", "Matern52Kernel", "RationalQuadraticKernel", "SignatureKernel",
-    "increment_tensor", "self_levels", "sig_kernel_dp", "sig_kernel_gram", "sig_levels_dp",
+    "increment_tensor", "self_levels", "sig_kernel_dp", "sig_kernel_gram", "sig_levels_dp", "sig_pde_kernel",
     "uses_fast_path", "median_heuristic", "SeedStream", "SequenceBatch", "gen_brownian", "ResourceCounters",
     "__version__",
 ]

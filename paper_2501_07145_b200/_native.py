@@ -24,7 +24,8 @@ PREC_CODES = {"fp32": 0, "fp64": 1}
 # every symbol include/sigkern_b200.h declares
 EXPORTS = ("sk_abi_version", "sk_last_error", "sk_workspace_bytes", "sk_fast_path",
            "sk_self_levels", "sk_gram", "sk_levels_dp_workspace_bytes", "sk_levels_dp",
-           "sk_increment_tensor", "sk_pairwise_dist")
+           "sk_increment_tensor", "sk_pairwise_dist", "sk_pde_workspace_bytes", "sk_pde_gram",
+           "sk_pde_self")
 
 
 class SkStaticSpec(ctypes.Structure):
@@ -64,6 +65,14 @@ def _declare(lib):
     lib.sk_levels_dp_workspace_bytes.argtypes = [I64, I64, I64, I32, I32]
     lib.sk_levels_dp.restype = ctypes.c_int
     lib.sk_levels_dp.argtypes = [P, I64, I64, I64, I32, I32, I32, P, P, SZ, P]
+    SPEC = ctypes.POINTER(SkStaticSpec)
+    lib.sk_pde_workspace_bytes.restype = SZ
+    lib.sk_pde_workspace_bytes.argtypes = [I64, I64, I32]
+    lib.sk_pde_gram.restype = ctypes.c_int
+    lib.sk_pde_gram.argtypes = [P, I64, I64, P, I64, I64, I64, I32, SPEC, I32, I64, I64, P, I64,
+                                P, SZ, P]
+    lib.sk_pde_self.restype = ctypes.c_int
+    lib.sk_pde_self.argtypes = [P, I64, I64, I64, SPEC, I32, P, P, SZ, P]
     lib.sk_pairwise_dist.restype = ctypes.c_int
     lib.sk_pairwise_dist.argtypes = [P, I64, I64, P, P]
     lib.sk_increment_tensor.restype = ctypes.c_int

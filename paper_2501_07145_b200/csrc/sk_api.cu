@@ -43,6 +43,22 @@ int check_config(const sk_kernel_config *c) {
   return SK_OK;
 }
 
+int check_static(const sk_static_spec *sp) {
+  if (!sp) return fail(SK_ERR_INVALID, "spec is NULL");
+  if (sp->kind < SK_LINEAR || sp->kind > SK_RATIONAL_QUADRATIC)
+    return fail(SK_ERR_INVALID, "unknown kernel kind " + std::to_string(sp->kind));
+  if (!(sp->scale > 0)) return fail(SK_ERR_INVALID, "scale must be positive");
+  if (sp->degree < 1) return fail(SK_ERR_INVALID, "degree must be a positive integer");
+  if (!(sp->bandwidth > 0)) return fail(SK_ERR_INVALID, "bandwidth must be positive");
+  if (!(sp->alpha > 0)) return fail(SK_ERR_INVALID, "alpha must be positive");
+  return SK_OK;
+}
+
+int check_pde_len(int64_t l, int difference) {
+  if (difference && l < 2) return fail(SK_ERR_INVALID, "pde kernel needs at least one increment per sequence");
+  return SK_OK;
+}
+
 int check_generic_limits(const sk_kernel_config &c) {
   if (c.n_levels > GEN_MAX_LEVELS)
     return fail(SK_ERR_UNSUPPORTED, "n_levels > " + std::to_string(GEN_MAX_LEVELS) +
@@ -187,6 +203,47 @@ int sk_pairwise_dist(const double *X, int64_t n, int64_t d, double *out, void *s
   if (n < 0 || d < 1) return fail(SK_ERR_INVALID, "expected (n, d) points with d >= 1");
   if (n > 1 && (!X || !out)) return fail(SK_ERR_INVALID, "NULL pointer");
   return pairwise_dist(X, n, d, out, (cudaStream_t)stream);
+}
+
+size_t sk_pde_workspace_bytes(int64_t npairs, int64_t ly, int32_t difference) {
+  return pde_workspace_bytes(npairs, ly, difference);
+}
+
+int sk_pde_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny, int64_t ly,
+                int64_t d, int32_t symmetric, const sk_static_spec *spec, int32_t difference,
+                int64_t row_begin, int64_t row_end, double *K, int64_t ldk, void *workspace,
+                size_t workspace_bytes, void *stream) {
+  clear_error();
+  int rc;
+  if ((rc = check_static(spec))) return rc;
+  if ((rc = check_batch(X, nx, lx, d, "X"))) return rc;
+  if (symmetric) {
+    Y = X;
+    ny = nx;
+    ly = lx;
+  } else if ((rc = check_batch(Y, ny, ly, d, "Y"))) {
+    return rc;
+  }
+  if ((rc = check_pde_len(lx, difference)) || (rc = check_pde_len(ly, difference))) return rc;
+  if (row_begin < 0 || row_end > nx || row_begin > row_end)
+    return fail(SK_ERR_INVALID, "row range outside [0, nx]");
+  if (!K) return fail(SK_ERR_INVALID, "K is NULL");
+  if (ldk < ny) return fail(SK_ERR_INVALID, "ldk < ny");
+  return pde_gram(X, nx, lx, Y, ny, ly, d, symmetric, *spec, difference, row_begin, row_end, K,
+                  ldk, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int sk_pde_self(const double *X, int64_t n, int64_t l, int64_t d, const sk_static_spec *spec,
+                int32_t difference, double *out, void *workspace, size_t workspace_bytes,
+                void *stream) {
+  clear_error();
+  int rc;
+  if ((rc = check_static(spec))) return rc;
+  if ((rc = check_batch(X, n, l, d, "X"))) return rc;
+  if ((rc = check_pde_len(l, difference))) return rc;
+  if (n > 0 && !out) return fail(SK_ERR_INVALID, "out is NULL");
+  return pde_self(X, n, l, d, *spec, difference, out, workspace, workspace_bytes,
+                  (cudaStream_t)stream);
 }
 
 }  // extern "C"

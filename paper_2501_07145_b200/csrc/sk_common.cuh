@@ -186,6 +186,15 @@ int tc_gemm_3xtf32(const float *Ahi, const float *Alo, int64_t Mtot, const float
                    const float *Blo, int64_t Ntot, int K, float *C, int64_t ldc, int64_t batch,
                    int64_t c_bstride, cudaStream_t st);
 
+// Goursat-PDE kernel (algorithm="pde"), float64.
+size_t pde_workspace_bytes(int64_t npairs, int64_t ly, int difference);
+int pde_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny, int64_t ly,
+             int64_t d, int symmetric, const sk_static_spec &sp, int difference,
+             int64_t row_begin, int64_t row_end, double *K, int64_t ldk, void *ws,
+             size_t ws_bytes, cudaStream_t st);
+int pde_self(const double *X, int64_t n, int64_t l, int64_t d, const sk_static_spec &sp,
+             int difference, double *out, void *ws, size_t ws_bytes, cudaStream_t st);
+
 // Upper-triangle pairwise distances (median_heuristic), float64.
 int pairwise_dist(const double *X, int64_t n, int64_t d, double *out, cudaStream_t st);
 

@@ -32,7 +32,7 @@ from .sequences import SequenceBatch
 from .utils import ResourceCounters, dp_flops
 
 __all__ = ["sig_kernel_gram", "sig_kernel_dp", "sig_levels_dp", "increment_tensor",
-           "self_levels", "uses_fast_path", "execution_path"]
+           "self_levels", "uses_fast_path", "execution_path", "sig_pde_kernel"]
 
 ALGORITHMS = ("dp", "pde", "bruteforce")  # kernels.py:53
 
@@ -212,9 +212,10 @@ def sig_kernel_gram(X, Y=None, cfg: KernelConfig = None, algorithm: str = "dp",
         raise ConfigError(
             "kernel.normalization: levelwise normalization requires level values; "
             "the pde algorithm supports none/global")
-    if algorithm != "dp":
+    if algorithm == "bruteforce":
         raise NotImplementedError(
-            f"algorithm={algorithm!r} is not part of the B200 build (only the dual DP path)")
+            "algorithm='bruteforce' is the reference's test oracle (kernels.py:218-249) and is "
+            "not part of the B200 build")
     if counters is None:
         counters = ResourceCounters()
     dev = X.device if isinstance(X, torch.Tensor) and X.is_cuda else _device(device)
@@ -224,9 +225,77 @@ def sig_kernel_gram(X, Y=None, cfg: KernelConfig = None, algorithm: str = "dp",
     dy = Xt.shape[2] if sym else Yt.shape[2]
     if Xt.shape[2] != dy:
         raise ValueError(f"channel mismatch: d={Xt.shape[2]} vs d={dy}")
+    if algorithm == "pde":
+        K = pde_gram_block(Xt, Yt, cfg)
+        return K.cpu().numpy() if was_np else K
     K, _ = gram_block(Xt, Yt, cfg, precision=precision)
     _count(counters, Xt, Yt, cfg, K)
     return K.cpu().numpy() if was_np else K
+
+
+# ---------------------------------------------------------------------------
+# algorithm="pde": untruncated signature kernel (kernels.py:334-507), float64
+# ---------------------------------------------------------------------------
+
+def _pde_self_t(Xt: torch.Tensor, cfg: KernelConfig) -> torch.Tensor:
+    lib = _native.load()
+    n, L, d = Xt.shape
+    out = torch.empty(n, dtype=torch.float64, device=Xt.device)
+    if n == 0:
+        return out
+    buf, nb = _workspace(lib.sk_pde_workspace_bytes(n, L, int(cfg.difference)), Xt.device)
+    sp = _native.static_struct(cfg.static)
+    with torch.cuda.device(Xt.device):
+        rc = lib.sk_pde_self(Xt.data_ptr(), n, L, d, sp, int(cfg.difference), out.data_ptr(),
+                             ctypes_ptr(buf), nb, _stream(Xt.device))
+    _native.check(rc, "sk_pde_self")
+    return out
+
+
+def pde_gram_block(Xt: torch.Tensor, Yt: torch.Tensor | None, cfg: KernelConfig) -> torch.Tensor:
+    """Goursat-PDE Gram on device tensors (the reference's _pde_gram + global
+    normalisation, kernels.py:559-571)."""
+    lib = _native.load()
+    sym = Yt is None
+    nx, lx, d = Xt.shape
+    Ys = Xt if sym else Yt
+    ny, ly = Ys.shape[0], Ys.shape[1]
+    if cfg.difference and (lx < 2 or ly < 2) and nx and ny:
+        raise ValueError("pde kernel needs at least one increment per sequence")
+    K = torch.zeros((nx, ny), dtype=torch.float64, device=Xt.device)
+    if nx and ny:
+        buf, nb = _workspace(lib.sk_pde_workspace_bytes(nx * ny, ly, int(cfg.difference)),
+                             Xt.device)
+        sp = _native.static_struct(cfg.static)
+        with torch.cuda.device(Xt.device):
+            rc = lib.sk_pde_gram(Xt.data_ptr(), nx, lx, Ys.data_ptr(), ny, ly, d, int(sym), sp,
+                                 int(cfg.difference), 0, nx, K.data_ptr(), ny, ctypes_ptr(buf),
+                                 nb, _stream(Xt.device))
+        _native.check(rc, "sk_pde_gram")
+    if cfg.normalization == "global":
+        sx = _pde_self_t(Xt, cfg)
+        sy = sx if sym else _pde_self_t(Yt, cfg)
+        for s in (sx, sy):  # kernels.py:519-527
+            bad = torch.nonzero(s <= 0).flatten()
+            if bad.numel():
+                raise NumericError(
+                    f"global normalization undefined: non-positive self-kernel for "
+                    f"input sequence index {int(bad[0])}")
+        K = K / torch.sqrt(sx[:, None] * sy[None, :])
+    return K
+
+
+def sig_pde_kernel(x, y, cfg: KernelConfig, counters=None, *, device=None) -> float:
+    """Untruncated signature kernel of one pair via the PDE solve (kernels.py:405-411)."""
+    dev = _device(device)
+    xt, _ = _as_pair_points(x, dev)
+    yt, _ = _as_pair_points(y, dev)
+    if xt.shape[1] != yt.shape[1]:
+        raise ValueError(f"dimension mismatch: {xt.shape[1]} vs {yt.shape[1]}")
+    K = pde_gram_block(xt[None], yt[None], KernelConfig(
+        static=cfg.static, n_levels=cfg.n_levels, order=cfg.order, difference=cfg.difference,
+        normalization="none"))
+    return float(K[0, 0])
 
 
 def _count(counters, Xt, Yt, cfg, K):

@@ -418,3 +418,61 @@ def test_normalised_gram_is_psd_on_fused_paths():
         assert uses_fast_path(40, 40, 3, cfg)
         K = sig_kernel_gram(X, cfg=cfg)
         assert np.linalg.eigvalsh(K).min() >= -1e-6
+
+
+# ---------------------------------------------------------------------------
+# algorithm="pde" (kernels.py:334-507): float64 Goursat solve on the device
+# ---------------------------------------------------------------------------
+
+def test_pde_golden_gram():
+    from test_oracle_golden import _pde_cases
+    for name, X, Y, sp, diff, norm, K_ref, kind, par in _pde_cases():
+        spec = StaticKernelSpec(kind=kind, **({"scale": par} if kind == "linear" else {"bandwidth": par}))
+        cfg = KernelConfig(static=spec, difference=diff, normalization=norm)
+        K = sig_kernel_gram(X, Y, cfg=cfg, algorithm="pde")
+        assert K.shape == K_ref.shape
+        assert np.allclose(K, K_ref, rtol=1e-11, atol=0), (name, _rel(K, K_ref))
+        if Y is None:
+            assert np.array_equal(K, K.T)
+
+
+def test_pde_hand_values_and_errors():
+    """test_kernels.py:233-262 re-pointed at the device path."""
+    from paper_2501_07145_b200 import sig_pde_kernel
+    x = np.ones((3, 2))
+    assert sig_pde_kernel(x, x, KernelConfig(static=LIN)) == 1.0
+    x = np.array([[0.0], [1.0]])
+    assert sig_pde_kernel(x, x, KernelConfig(static=LIN)) == pytest.approx(2.0)
+    with pytest.raises(ValueError, match="increment"):
+        sig_pde_kernel(np.array([[1.0]]), np.array([[1.0]]), KernelConfig(static=LIN))
+    one = np.array([[1.0]])
+    assert sig_pde_kernel(one, one, KernelConfig(static=LIN, difference=False)) == pytest.approx(2.0)
+
+
+def test_pde_second_order_convergence():
+    """test_acceptance.py:103-125: dyadic refinement of the unit linear path converges
+    to sum 1/(m!)^2 with error ratios in [3, 6]."""
+    import math
+    from paper_2501_07145_b200 import sig_pde_kernel
+    target = sum(1.0 / math.factorial(m) ** 2 for m in range(30))
+    errs = []
+    for r in range(9):
+        path = np.linspace(0.0, 1.0, 2 ** r + 1)[:, None]
+        errs.append(abs(sig_pde_kernel(path, path, KernelConfig(static=LIN)) - target))
+    ratios = [errs[i] / errs[i + 1] for i in range(len(errs) - 1)]
+    assert all(3.0 <= q <= 6.0 for q in ratios[2:]), ratios
+
+
+def test_pde_vs_truncated_consistency():
+    """test_acceptance.py:128-145: PDE ~ truncated M=10, p=5 kernel at small increments."""
+    from paper_2501_07145_b200 import sig_pde_kernel
+    cfg = KernelConfig(static=StaticKernelSpec(kind="rbf", bandwidth=2.0), n_levels=10, order=5)
+    rng = np.random.default_rng(0)
+    worst = 0.0
+    for _ in range(10):
+        X = np.vstack([np.zeros((1, 2)), np.cumsum(0.1 * rng.standard_normal((5, 2)), axis=0)])
+        Y = np.vstack([np.zeros((1, 2)), np.cumsum(0.1 * rng.standard_normal((5, 2)), axis=0)])
+        pde = sig_pde_kernel(X, Y, cfg)
+        dp = sig_kernel_dp(X, Y, cfg, precision="fp64").total()
+        worst = max(worst, abs(pde - dp) / abs(pde))
+    assert worst <= 1e-3, worst

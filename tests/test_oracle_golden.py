@@ -85,3 +85,22 @@ def test_oracle_median_heuristic_golden():
     for name in sorted({k.split("__")[0] for k in z.files}):
         got = O.median_heuristic(z[f"{name}__X"], max_pairs=int(z[f"{name}__max_pairs"]))
         assert got == float(z[f"{name}__median"]), name  # same numpy ops: bitwise
+
+
+def _pde_cases():
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "pde.npz"))
+    for name in sorted({k.split("__")[0] for k in z.files}):
+        kind = str(z[f"{name}__kind"])
+        par = float(z[f"{name}__param"])
+        sp = O.static_params(kind, **({"scale": par} if kind == "linear" else {"bandwidth": par}))
+        Y = z[f"{name}__Y"] if f"{name}__Y" in z.files else None
+        yield name, z[f"{name}__X"], Y, sp, bool(z[f"{name}__diff"]), str(z[f"{name}__norm"]), \
+            z[f"{name}__K"], kind, par
+
+
+def test_oracle_pde_golden():
+    """The oracle's row-streamed PDE restatement reproduces the reference (kernels.py:334-507)."""
+    for name, X, Y, sp, diff, norm, K, _, _ in _pde_cases():
+        got = O.pde_gram(X, Y, sp=sp, difference=diff, normalization=norm)
+        assert np.allclose(got, K, rtol=1e-12, atol=0), name
