@@ -283,8 +283,8 @@ int fast_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
   Params P = base_params(pl, pk);
   P.nx = P.ny = n;
   P.tiles_y = (n + pl.segs - 1) / pl.segs;
-  P.ntiles = P.tiles_y;
-  P.rx = pl.segs;
+  P.ntiles = n;  // one tile per sequence (diag mode)
+  P.rx = 1;
   P.row_begin = 0;
   P.row_end = n;
   P.diag_mode = 1;

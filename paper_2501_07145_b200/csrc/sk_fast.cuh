@@ -618,11 +618,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) gram_kernel(const Params P) {
   for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x) {
     const int64_t ty = tile % P.tiles_y;
     const int64_t tx = tile / P.tiles_y;
-    const int64_t ybase = ty * P.segs;
+    int64_t ybase = ty * P.segs;
     int64_t x0, njobs;
     if (P.diag_mode) {
-      x0 = ybase;
-      njobs = min((int64_t)P.segs, P.ny - x0);
+      // self levels: one tile per sequence t; the CTA streams x_t once and
+      // only the segment holding y_t keeps its (diagonal) pair
+      ybase = (tile / P.segs) * P.segs;
+      x0 = tile;
+      njobs = 1;
     } else {
       x0 = P.row_begin + tx * P.rx;
       njobs = min((int64_t)P.rx, P.row_end - x0);

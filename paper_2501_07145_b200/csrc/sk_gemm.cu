@@ -46,11 +46,14 @@ __global__ void __launch_bounds__(NTHREADS) gemm_dp_kernel(const Params P) {
   for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x) {
     const int64_t ty = tile % P.tiles_y;
     const int64_t tx = tile / P.tiles_y;
-    const int64_t ybase = ty * P.segs;
+    int64_t ybase = ty * P.segs;
     int64_t x0, njobs;
     if (P.diag_mode) {
-      x0 = ybase;
-      njobs = min((int64_t)P.segs, P.ny - x0);
+      // self levels: one tile per sequence t; the CTA streams x_t once and
+      // only the segment holding y_t keeps its (diagonal) pair
+      ybase = (tile / P.segs) * P.segs;
+      x0 = tile;
+      njobs = 1;
     } else {
       x0 = P.row_begin + tx * P.rx;
       njobs = min((int64_t)P.rx, P.row_end - x0);
@@ -451,8 +454,8 @@ int gemm_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
   Params P = base_params(pl, l, carry);
   P.nx = P.ny = n;
   P.tiles_y = (n + pl.segs - 1) / pl.segs;
-  P.ntiles = P.tiles_y;
-  P.rx = pl.segs;
+  P.ntiles = n;  // one tile per sequence (diag mode)
+  P.rx = 1;
   P.row_begin = 0;
   P.row_end = n;
   P.diag_mode = 1;

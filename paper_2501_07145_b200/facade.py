@@ -72,7 +72,8 @@ class SignatureKernel:
 
     def __init__(self, n_levels: int = 5, order: int | None = 1, normalize: bool = True,
                  difference: bool = True, static_kernel: StaticKernel | None = None,
-                 normalization: str | None = None, precision: str = "fp32", device=None):
+                 normalization: str | None = None, precision: str = "fp32", device=None,
+                 cuda_graph: bool = False):
         static_kernel = static_kernel if static_kernel is not None else RBFKernel()
         if normalization is None:
             normalization = "levelwise" if normalize else "none"
@@ -81,6 +82,10 @@ class SignatureKernel:
                                    difference=difference, normalization=normalization)
         self.precision = precision
         self.device = device
+        # cuda_graph=True: repeated calls with the same shapes replay a captured
+        # CUDA graph (plan.GramPlan) instead of re-issuing launches from Python
+        self.cuda_graph = cuda_graph
+        self._plans = {}
 
     @property
     def n_levels(self) -> int:
@@ -97,6 +102,14 @@ class SignatureKernel:
     def __call__(self, X, Y=None, diag: bool = False):
         if diag:
             return self.diag(X)
+        if self.cuda_graph:
+            from .plan import GramPlan
+            key = (tuple(X.shape), None if Y is None else tuple(Y.shape))
+            plan = self._plans.get(key)
+            if plan is None:
+                plan = self._plans[key] = GramPlan(self.config, key[0], key[1],
+                                                   precision=self.precision, device=self.device)
+            return plan(X, Y)
         return sig_kernel_gram(X, Y, cfg=self.config, precision=self.precision,
                                device=self.device)
 

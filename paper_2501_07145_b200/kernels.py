@@ -140,7 +140,8 @@ def _self_levels_t(Xt: torch.Tensor, cfg: KernelConfig, precision: str,
 
 def gram_block(Xt: torch.Tensor, Yt: torch.Tensor | None, cfg: KernelConfig,
                row_begin: int = 0, row_end: int | None = None, precision: str = "fp32",
-               diag_x=None, diag_y=None, K=None, want_levels: bool = False):
+               diag_x=None, diag_y=None, K=None, want_levels: bool = False,
+               check_global: bool = True):
     """Rows [row_begin, row_end) of the Gram on device tensors (the sk_gram call).
 
     Yt=None is the symmetric K(X): K must then be the full (N, N) matrix (it is
@@ -161,7 +162,7 @@ def gram_block(Xt: torch.Tensor, Yt: torch.Tensor | None, cfg: KernelConfig,
             diag_x = _self_levels_t(Xt, cfg, precision, c, ws)
         if diag_y is None:
             diag_y = diag_x if sym else _self_levels_t(Yt, cfg, precision, c, ws)
-        if cfg.normalization == "global":
+        if cfg.normalization == "global" and check_global:
             _check_global(diag_x, diag_y)
     rows = nx if sym else row_end - row_begin
     if K is None:

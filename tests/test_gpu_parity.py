@@ -476,3 +476,52 @@ def test_pde_vs_truncated_consistency():
         dp = sig_kernel_dp(X, Y, cfg, precision="fp64").total()
         worst = max(worst, abs(pde - dp) / abs(pde))
     assert worst <= 1e-3, worst
+
+
+# ---------------------------------------------------------------------------
+# CUDA-graph plans (plan.GramPlan / SignatureKernel(cuda_graph=True))
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("norm", ["levelwise", "none", "global"])
+def test_graph_plan_matches_eager_bitwise(norm):
+    import time
+    from paper_2501_07145_b200 import RBFKernel, SignatureKernel
+    X = gen_brownian(64, 50, 3, SeedStream(1)).data
+    Y = gen_brownian(48, 50, 3, SeedStream(2)).data
+    eager = SignatureKernel(n_levels=5, normalization=norm, static_kernel=RBFKernel())
+    graph = SignatureKernel(n_levels=5, normalization=norm, static_kernel=RBFKernel(),
+                            cuda_graph=True)
+    for A, B in ((X, None), (X, Y)):
+        want = eager(A, B)
+        assert np.array_equal(graph(A, B), want)
+        A2 = A + 0.01  # same plan, new inputs
+        assert np.array_equal(graph(A2, B), eager(A2, B))
+    Xt = torch.from_numpy(X).cuda()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(50):
+        Kg = graph(Xt)
+    torch.cuda.synchronize()
+    tg = (time.perf_counter() - t0) / 50
+    t0 = time.perf_counter()
+    for _ in range(50):
+        Ke = eager(Xt)
+    torch.cuda.synchronize()
+    te = (time.perf_counter() - t0) / 50
+    assert torch.equal(Kg, Ke)
+    print(f"c1 K(X) {norm}: graph {1e6 * tg:.0f} us/call, eager {1e6 * te:.0f} us/call")
+
+
+def test_graph_plan_errors():
+    from paper_2501_07145_b200.plan import GramPlan
+    plan = GramPlan(KernelConfig(n_levels=3, normalization="global"), (4, 10, 2))
+    X = gen_brownian(4, 10, 2, SeedStream(3)).data
+    plan(X)
+    bad = X.copy()
+    bad[1, 3, 0] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        plan(bad)
+    with pytest.raises(ValueError, match="shape"):
+        plan(X[:3])
+    const = np.zeros((4, 10, 2))  # zero self-kernels beyond level 0 are fine (level 0 = 1)
+    plan(const)
