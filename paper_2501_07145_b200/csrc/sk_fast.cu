@@ -69,7 +69,13 @@ struct Plan {
   bool ok = false;
   int D = 0, C = 8, sw = 0, segs = 0, npanel = 1, nhp = 0;
   bool linear = false;
+  int variant = 0;  // 0 rbf, 1 linear, 2 stationary kinds (matern*, rational quadratic)
 };
+
+bool stationary_kind(int kind) {
+  return kind == SK_MATERN12 || kind == SK_MATERN32 || kind == SK_MATERN52 ||
+         kind == SK_RATIONAL_QUADRATIC;
+}
 
 int next_pow2(int v) {
   int p = 1;
@@ -85,7 +91,9 @@ Plan plan_for(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   Plan pl;
   const int kind = c.static_spec.kind;
   if (c.precision != SK_PREC_FP32 || !c.difference) return pl;
-  if (kind != SK_RBF && kind != SK_LINEAR) return pl;
+  const bool stat = stationary_kind(kind);
+  if (kind != SK_RBF && kind != SK_LINEAR && !stat) return pl;  // polynomial: float64 kernel
+  if (stat && c.order != 1) return pl;  // stationary kinds: order-1 kernels only
   if (!fast_orders_supported(c.n_levels, c.order)) return pl;
   // Normalised linear kernels of order > 1 are sensitive to the FP32
   // accumulation of the increment inner products (measured 1.6-2.1e-5 vs the
@@ -111,6 +119,7 @@ Plan plan_for(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   if (((size_t)NSLOT * lx2 + 1) * x_stride(pl.D) * sizeof(float) > SMEM_LIMIT) return pl;
   pl.segs = NWARPS * (32 / pl.sw);
   pl.linear = kind == SK_LINEAR;
+  pl.variant = pl.linear ? 1 : (stat ? 2 : 0);
   pl.ok = true;
   return pl;
 }
@@ -137,6 +146,7 @@ size_t roles_bytes(int64_t nx, int64_t lx, int64_t ny, const Plan &pl) {
 
 double coord_scale(const sk_kernel_config &c) {
   if (c.static_spec.kind == SK_LINEAR) return std::sqrt(c.static_spec.scale);
+  if (stationary_kind(c.static_spec.kind)) return 1.0 / c.static_spec.bandwidth;  // r = |x'-y'|
   // G = exp(-|x-y|^2 / (2 bw^2)) = exp2(-|x'-y'|^2 / 2) with x' = x sqrt(log2 e) / bw
   return std::sqrt(1.4426950408889634) / c.static_spec.bandwidth;
 }
@@ -150,11 +160,11 @@ int launch(const Params &P, const Plan &pl, int M, int order, cudaStream_t st) {
   const size_t smem = ((size_t)NSLOT * P.lx2 + 1) * x_stride(pl.D) * sizeof(float);
   switch (pl.D) {
     case 4:
-      return launch_d4(P, M, order, pl.linear, smem, st);
+      return launch_d4(P, M, order, pl.variant, smem, st);
     case 8:
-      return launch_d8(P, M, order, pl.linear, smem, st);
+      return launch_d8(P, M, order, pl.variant, smem, st);
     case 16:
-      return launch_d16(P, M, order, pl.linear, smem, st);
+      return launch_d16(P, M, order, pl.variant, smem, st);
     default:
       return fail(SK_ERR_UNSUPPORTED, "fast path: unsupported channel padding");
   }
@@ -198,8 +208,10 @@ int pack_roles(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t
   return SK_OK;
 }
 
-Params base_params(const Plan &pl, const Packed &pk) {
+Params base_params(const Plan &pl, const Packed &pk, const sk_kernel_config &c) {
   Params P{};
+  P.static_kind = c.static_spec.kind;
+  P.rq_alpha = (float)c.static_spec.alpha;
   P.xs = pk.xs;
   P.ys = pk.ys;
   P.lx2 = pk.lx2;
@@ -245,7 +257,7 @@ int fast_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t 
   Packed pk{};
   int rc = pack_roles(X, nx, lx, Y, ny, ly, d, pl, c, ws, ws_bytes, st, pk);
   if (rc) return rc;
-  Params P = base_params(pl, pk);
+  Params P = base_params(pl, pk, c);
   P.nx = nx;
   P.ny = ny;
   P.tiles_y = (ny + pl.segs - 1) / pl.segs;
@@ -280,7 +292,7 @@ int fast_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
   if (rc) return rc;
   // each CTA evaluates its segments' y against the same sequences as x and
   // keeps the diagonal: the same kernel and arithmetic as the Gram's diagonal
-  Params P = base_params(pl, pk);
+  Params P = base_params(pl, pk, c);
   P.nx = P.ny = n;
   P.tiles_y = (n + pl.segs - 1) / pl.segs;
   P.ntiles = n;  // one tile per sequence (diag mode)

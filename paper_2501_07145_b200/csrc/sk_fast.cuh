@@ -97,6 +97,9 @@ struct Params {
   float *carry;  // [max_ctas * NWARPS][rx + 2 jobs][lx2 steps][nhp]
   int nhp;       // floats per carry entry (2 x NCA chain values, 2 x lastD, kout; padded to 4)
   int max_ctas;  // grid size the carry buffer was sized for
+  // stationary static kinds (StatPointStage): kind and rational-quadratic alpha
+  int static_kind;
+  float rq_alpha;
   // GEMM-fed path (sk_gemm.cu): pair (x, y) row r of the cell matrix is at
   // S + (x - x_blk0) * s_xstride + y * s_ystride + r * s_ld
   const float *S;
@@ -122,6 +125,11 @@ __device__ __forceinline__ void unpack2(u64 v, float &lo, float &hi) {
 __device__ __forceinline__ u64 ffma2_bc(u64 a, float b, u64 c) {
   u64 d;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(pack2(b, b)), "l"(c));
+  return d;
+}
+__device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) {
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
   return d;
 }
 __device__ __forceinline__ u64 fadd2_bc(u64 a, float b) {
@@ -253,6 +261,8 @@ struct PointStage {
   float lastDa, lastDb;
   float ga[C], gb[C];  // point-kernel rows a, b of the current row pair
 
+  __device__ __forceinline__ void configure(const Params &) {}
+
   // this lane's columns of the packed y sequence (pre-scaled points, n-terms)
   __device__ __forceinline__ void load_y(const float *__restrict__ yp) {
 #pragma unroll
@@ -314,6 +324,99 @@ struct PointStage {
 };
 
 // ---------------------------------------------------------------------------
+// Stationary static kinds (static/kernels.py:74-89): Matern 1/2, 3/2, 5/2 and
+// rational quadratic, k = f(r), r = |x - y| / bandwidth. Coordinates are
+// pre-scaled by 1/bandwidth and the squared distance is formed from DIRECT
+// differences, sum_k (x_k - y_k)^2 (packed FADD2 + FFMA2 per channel): the
+// norm expansion that the rbf stage uses would put an absolute error of
+// ~eps |x|^2 under the square root (Matern 1/2 levelwise: 1.2e-4 in a numpy
+// FP32 emulation vs 5.7e-8 with direct differences). The kind is a
+// warp-uniform runtime parameter.
+// ---------------------------------------------------------------------------
+template <int D, int C_>
+struct StatPointStage {
+  static constexpr int C = C_;
+  static constexpr int XP = x_stride(D);
+  static constexpr int YP = y_stride(D);
+
+  float ynv[C][D];  // -y (negated: the difference is one FADD2 with a broadcast operand)
+  float prevG[C];
+  float lastDa, lastDb;
+  float ga[C], gb[C];
+  int kind;
+  float alpha, inv2a;
+
+  __device__ __forceinline__ void configure(const Params &P) {
+    kind = P.static_kind;
+    alpha = P.rq_alpha;
+    inv2a = 0.5f / P.rq_alpha;
+  }
+  __device__ __forceinline__ void load_y(const float *__restrict__ yp) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+#pragma unroll
+      for (int k4 = 0; k4 < D / 4; ++k4) {
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(yp + c * YP) + k4);
+        ynv[c][4 * k4 + 0] = -v.x;
+        ynv[c][4 * k4 + 1] = -v.y;
+        ynv[c][4 * k4 + 2] = -v.z;
+        ynv[c][4 * k4 + 3] = -v.w;
+      }
+      prevG[c] = 0.f;
+    }
+    lastDa = lastDb = 0.f;
+  }
+  __device__ __forceinline__ float kfun(float sq) const {
+    constexpr float L2E = 1.4426950408889634f;
+    float sr;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sr) : "f"(sq));
+    if (kind == SK_MATERN12) return ex2_approx(-L2E * sr);
+    if (kind == SK_MATERN32) {
+      const float t = 1.7320508075688772f * sr;
+      return (1.f + t) * ex2_approx(-L2E * t);
+    }
+    if (kind == SK_MATERN52) {
+      const float t = 2.23606797749979f * sr;
+      return fmaf(t * t, 1.f / 3.f, 1.f + t) * ex2_approx(-L2E * t);
+    }
+    // rational quadratic: (1 + sq / (2 alpha))^(-alpha)
+    float lg;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(fmaf(sq, inv2a, 1.f)));
+    return ex2_approx(-alpha * lg);
+  }
+  __device__ __forceinline__ void point(const float *__restrict__ xptr) {
+    u64 acc[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[c] = 0ull;
+    const float4 *xr = reinterpret_cast<const float4 *>(xptr);
+#pragma unroll
+    for (int k2 = 0; k2 < D / 2; ++k2) {
+      const float4 v = xr[k2];
+      const u64 p0 = pack2(v.x, v.y);
+      const u64 p1 = pack2(v.z, v.w);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const u64 d0 = fadd2_bc(p0, ynv[c][2 * k2]);
+        const u64 d1 = fadd2_bc(p1, ynv[c][2 * k2 + 1]);
+        acc[c] = ffma2(d0, d0, acc[c]);
+        acc[c] = ffma2(d1, d1, acc[c]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      float lo, hi;
+      unpack2(acc[c], lo, hi);
+      ga[c] = kfun(lo);
+      gb[c] = kfun(hi);
+    }
+  }
+  __device__ __forceinline__ void increments(float dla, float dlb, bool zero_left, float (&aa)[C],
+                                             float (&ab)[C]) {
+    double_difference<C, false>(ga, gb, prevG, lastDa, lastDb, dla, dlb, zero_left, aa, ab);
+  }
+};
+
+// ---------------------------------------------------------------------------
 // GEMM-fed stage (large d, sk_gemm.cu): the exponent (rbf, with the n-terms
 // folded into the GEMM's K) or the increment inner product (linear) of every
 // cell was produced by a library GEMM into HBM; a row pair is two rows of
@@ -327,6 +430,7 @@ struct GemmStage {
   float ga[C], gb[C];
   int64_t ld;
 
+  __device__ __forceinline__ void configure(const Params &P) { ld = P.s_ld; }
   __device__ __forceinline__ void reset_y() {
 #pragma unroll
     for (int c = 0; c < C; ++c) prevG[c] = 0.f;
@@ -615,6 +719,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gram_kernel(const Params P) {
   const bool first_lane = (q == 0);
 
   LS st;
+  st.configure(P);
   for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x) {
     const int64_t ty = tile % P.tiles_y;
     const int64_t tx = tile / P.tiles_y;
@@ -732,9 +837,9 @@ __global__ void pack_x_kernel(const double *__restrict__ X, int64_t n, int64_t L
                               int64_t Lp2, int D, double coord_scale, int incr,
                               float *__restrict__ out);
 
-int launch_d4(const Params &, int M, int order, int linear, size_t smem, cudaStream_t st);
-int launch_d8(const Params &, int M, int order, int linear, size_t smem, cudaStream_t st);
-int launch_d16(const Params &, int M, int order, int linear, size_t smem, cudaStream_t st);
+int launch_d4(const Params &, int M, int order, int variant, size_t smem, cudaStream_t st);
+int launch_d8(const Params &, int M, int order, int variant, size_t smem, cudaStream_t st);
+int launch_d16(const Params &, int M, int order, int variant, size_t smem, cudaStream_t st);
 
 // Compiled (n_levels, order) combinations: order 1 with n_levels 1..8, and
 // the geometric kernel order = n_levels for n_levels 2..5.
@@ -760,6 +865,7 @@ int launch_kernel(const Params &P, size_t smem, cudaStream_t st) {
   return SK_OK;
 }
 
+// variant: 0 rbf, 1 linear, 2 stationary kinds (StatPointStage, order 1 only)
 template <int D, bool LIN>
 int launch_impl_lin(const Params &P, int M, int order, size_t smem, cudaStream_t st) {
   if (order == 1) {
@@ -786,11 +892,30 @@ int launch_impl_lin(const Params &P, int M, int order, size_t smem, cudaStream_t
   return fail(SK_ERR_UNSUPPORTED, "fast path: (n_levels, order) not compiled");
 }
 
+template <int D>
+int launch_impl_stat(const Params &P, int M, int order, size_t smem, cudaStream_t st) {
+  if (order == 1) {
+    switch (M) {
+      case 1: return launch_kernel<LaneState1<StatPointStage<D, 8>, 1>>(P, smem, st);
+      case 2: return launch_kernel<LaneState1<StatPointStage<D, 8>, 2>>(P, smem, st);
+      case 3: return launch_kernel<LaneState1<StatPointStage<D, 8>, 3>>(P, smem, st);
+      case 4: return launch_kernel<LaneState1<StatPointStage<D, 8>, 4>>(P, smem, st);
+      case 5: return launch_kernel<LaneState1<StatPointStage<D, 8>, 5>>(P, smem, st);
+      case 6: return launch_kernel<LaneState1<StatPointStage<D, 8>, 6>>(P, smem, st);
+      case 7: return launch_kernel<LaneState1<StatPointStage<D, 8>, 7>>(P, smem, st);
+      case 8: return launch_kernel<LaneState1<StatPointStage<D, 8>, 8>>(P, smem, st);
+      default: break;
+    }
+  }
+  return fail(SK_ERR_UNSUPPORTED, "fast path: stationary kinds are compiled for order 1");
+}
+
 // Instantiation helper shared by the per-D translation units.
 template <int D>
-int launch_impl(const Params &P, int M, int order, int linear, size_t smem, cudaStream_t st) {
-  return linear ? launch_impl_lin<D, true>(P, M, order, smem, st)
-                : launch_impl_lin<D, false>(P, M, order, smem, st);
+int launch_impl(const Params &P, int M, int order, int variant, size_t smem, cudaStream_t st) {
+  if (variant == 2) return launch_impl_stat<D>(P, M, order, smem, st);
+  return variant == 1 ? launch_impl_lin<D, true>(P, M, order, smem, st)
+                      : launch_impl_lin<D, false>(P, M, order, smem, st);
 }
 
 }  // namespace fast

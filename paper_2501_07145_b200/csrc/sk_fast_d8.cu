@@ -3,8 +3,8 @@
 
 namespace sk {
 namespace fast {
-int launch_d8(const Params &P, int M, int order, int linear, size_t smem, cudaStream_t st) {
-  return launch_impl<8>(P, M, order, linear, smem, st);
+int launch_d8(const Params &P, int M, int order, int variant, size_t smem, cudaStream_t st) {
+  return launch_impl<8>(P, M, order, variant, smem, st);
 }
 }  // namespace fast
 }  // namespace sk

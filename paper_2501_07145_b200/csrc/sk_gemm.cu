@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(NTHREADS) gemm_dp_kernel(const Params P) {
   const int64_t rowpair = 2 * P.s_ld;  // floats between row pairs
 
   LS st;
-  st.ld = P.s_ld;
+  st.configure(P);
   for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x) {
     const int64_t ty = tile % P.tiles_y;
     const int64_t tx = tile / P.tiles_y;

@@ -53,7 +53,12 @@ def test_fast_path_selection():
     f64 = _native.config_struct(KernelConfig(n_levels=5), "fp64")
     assert lib.sk_fast_path(256, 256, 16, f64) == 0
     mat = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="matern32")))
-    assert lib.sk_fast_path(64, 64, 4, mat) == 0
+    assert lib.sk_fast_path(64, 64, 4, mat) == 1            # stationary kinds, order 1: fused
+    matp = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="matern32"), n_levels=3,
+                                              order=3))
+    assert lib.sk_fast_path(64, 64, 4, matp) == 0           # stationary kinds, order > 1: float64
+    poly = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="polynomial")))
+    assert lib.sk_fast_path(64, 64, 4, poly) == 0           # polynomial: float64
     assert lib.sk_fast_path(300, 300, 4, c3) == 1           # two 256-column panels
     assert lib.sk_fast_path(2048, 2048, 4, _native.config_struct(KernelConfig(n_levels=8))) == 1  # c5
     assert lib.sk_fast_path(1000, 1000, 16, c3) == 2        # x ring would exceed shared memory

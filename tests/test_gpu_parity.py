@@ -525,3 +525,36 @@ def test_graph_plan_errors():
         plan(X[:3])
     const = np.zeros((4, 10, 2))  # zero self-kernels beyond level 0 are fine (level 0 = 1)
     plan(const)
+
+
+# ---------------------------------------------------------------------------
+# stationary static kinds on the fused FP32 kernel (StatPointStage)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("kind", ["matern12", "matern32", "matern52", "rational_quadratic"])
+def test_stationary_kinds_fused(kind):
+    X = gen_brownian(7, 60, 5, SeedStream(51)).data
+    Y = gen_brownian(6, 45, 5, SeedStream(52)).data
+    extra = dict(alpha=1.7) if kind == "rational_quadratic" else {}
+    spec = StaticKernelSpec(kind=kind, bandwidth=0.9, **extra)
+    sp = O.static_params(kind, bandwidth=0.9, **extra)
+    for norm, tol in (("none", TOL_RAW), ("levelwise", TOL_NORM), ("global", TOL_NORM)):
+        cfg = KernelConfig(static=spec, n_levels=5, normalization=norm)
+        assert uses_fast_path(60, 45, 5, cfg)
+        R = O.gram(X, Y, sp=sp, M=5, p=1, normalization=norm)
+        assert _scaled_err(sig_kernel_gram(X, Y, cfg=cfg), R) <= tol, (kind, norm)
+    cfg = KernelConfig(static=spec, n_levels=4, normalization="levelwise")
+    K = sig_kernel_gram(X, cfg=cfg)
+    assert np.array_equal(K, K.T) and np.array_equal(np.diag(K), np.ones(7))
+    assert _scaled_err(K, O.gram(X, None, sp=sp, M=4, p=1, normalization="levelwise")) <= TOL_NORM
+
+
+def test_stationary_kind_multi_panel():
+    X = gen_brownian(4, 300, 3, SeedStream(53)).data
+    Y = gen_brownian(3, 280, 3, SeedStream(54)).data
+    spec = StaticKernelSpec(kind="matern32", bandwidth=1.2)
+    cfg = KernelConfig(static=spec, n_levels=4, normalization="levelwise")
+    assert uses_fast_path(300, 280, 3, cfg)
+    R = O.gram(X, Y, sp=O.static_params("matern32", bandwidth=1.2), M=4, p=1,
+               normalization="levelwise")
+    assert _scaled_err(sig_kernel_gram(X, Y, cfg=cfg), R) <= TOL_NORM
