@@ -45,8 +45,12 @@ namespace tc {
 
 constexpr int BM = 128;          // tile rows (A side, TMEM lanes)
 constexpr int BN = 256;          // tile columns (B side, TMEM columns)
-constexpr int KC = 32;           // K floats per stage (one 128-byte swizzle atom row)
-constexpr int STAGES = 2;
+#ifndef SK_TC_KC
+#define SK_TC_KC 32
+#endif
+constexpr int KC = SK_TC_KC;     // K floats per stage (one swizzle atom row: 128 or 64 bytes)
+constexpr int STAGES = 2 * 32 / KC;
+constexpr int SWZ_BYTES = KC * 4;  // swizzle atom width
 constexpr int A_BYTES = BM * KC * 4;  // 16 KB per part
 constexpr int B_BYTES = BN * KC * 4;  // 32 KB per part
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
@@ -92,14 +96,15 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
-// shared-memory matrix descriptor: K-major, 128B swizzle, 8-row groups 1024 B apart
+// shared-memory matrix descriptor: K-major, 128B (or 64B) swizzle, 8-row
+// groups 8 * SWZ_BYTES apart
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
-  d |= (uint64_t)1 << 16;                           // leading byte offset (unused for SW128 K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;                 // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1 << 16;                           // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)((8 * SWZ_BYTES) >> 4) << 32;      // stride byte offset: 8 rows x atom width
   d |= (uint64_t)1 << 46;                           // descriptor version (sm_100)
-  d |= (uint64_t)2 << 61;                           // layout: SWIZZLE_128B
+  d |= (uint64_t)(SWZ_BYTES == 128 ? 2 : 4) << 61;  // layout: SWIZZLE_128B / SWIZZLE_64B
   return d;
 }
 // instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = 256
@@ -307,7 +312,8 @@ int make_map(CUtensorMap *map, const float *base, int64_t rows, int K, int64_t b
   cuuint32_t box[3] = {(cuuint32_t)KC, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)base, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  SWZ_BYTES == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return SK_OK;
