@@ -7,18 +7,38 @@
 namespace sk {
 namespace fast {
 
-// coordinate k of packed point r (rows beyond L repeat the last point);
-// incr: the increment x_r - x_{r-1} instead (0 for r = 0 and beyond L)
+// Packed value of channel k at packed index r of one sequence, and whether
+// the slot is a dummy (point kernel 0). mode: 0 points (rows beyond L repeat
+// the last point: zero increments); 1 increments x_r - x_{r-1} (0 for r = 0
+// and beyond L); 2/3 difference=False (rbf / linear), x role: row 0 and rows
+// beyond L are dummies, row r holds point r-1; y role: point r, dummies
+// beyond L.
 __device__ __forceinline__ double packed_coord(const double *__restrict__ seq, int64_t L,
-                                               int64_t d, int64_t r, int k, int incr) {
+                                               int64_t d, int64_t r, int k, int mode,
+                                               bool xrole, bool &dummy) {
+  dummy = false;
+  if (mode >= 2) {
+    const int64_t pt = xrole ? r - 1 : r;
+    if (pt < 0 || pt >= L) {
+      dummy = true;
+      return 0.0;
+    }
+    return seq[pt * d + k];
+  }
   const int64_t pt = min(r, L - 1);
   double v = seq[pt * d + k];
-  if (incr) v = (r >= 1 && r < L) ? v - seq[(pt - 1) * d + k] : 0.0;
+  if (mode == 1) v = (r >= 1 && r < L) ? v - seq[(pt - 1) * d + k] : 0.0;
   return v;
 }
 
+// n-term slot: -|x'|^2/2 for the rbf modes (-1e30 for dummies), 0 for linear
+__device__ __forceinline__ float nterm(int mode, double nrm, bool dummy) {
+  if (mode == 1 || mode == 3) return 0.f;
+  return dummy ? -1e30f : (float)(-0.5 * nrm);
+}
+
 __global__ void pack_y_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
-                              int64_t Lp, int D, double coord_scale, int incr,
+                              int64_t Lp, int D, double coord_scale, int mode,
                               float *__restrict__ out) {
   const int YP = y_stride(D);
   const int64_t total = n * Lp;
@@ -28,18 +48,21 @@ __global__ void pack_y_kernel(const double *__restrict__ X, int64_t n, int64_t L
     const double *seq = X + s * L * d;
     float *dst = out + t * YP;
     double nrm = 0.0;
+    bool dummy = false;
     for (int k = 0; k < D; ++k) {
-      const float v = (k < d) ? (float)(packed_coord(seq, L, d, t % Lp, k, incr) * coord_scale) : 0.f;
+      const float v =
+          (k < d) ? (float)(packed_coord(seq, L, d, t % Lp, k, mode, false, dummy) * coord_scale)
+                  : 0.f;
       dst[k] = v;
       nrm += (double)v * (double)v;  // n-term from the rounded coordinates
     }
-    dst[D] = incr ? 0.f : (float)(-0.5 * nrm);
+    dst[D] = nterm(mode, nrm, dummy);
     for (int k = D + 1; k < YP; ++k) dst[k] = 0.f;
   }
 }
 
 __global__ void pack_x_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
-                              int64_t Lp2, int D, double coord_scale, int incr,
+                              int64_t Lp2, int D, double coord_scale, int mode,
                               float *__restrict__ out) {
   const int XP = x_stride(D);
   const int64_t total = n * Lp2 * 2;  // one thread per (sequence, row)
@@ -51,12 +74,14 @@ __global__ void pack_x_kernel(const double *__restrict__ X, int64_t n, int64_t L
     const double *seq = X + s * L * d;
     float *dst = out + (s * Lp2 + (r >> 1)) * XP;
     double nrm = 0.0;
+    bool dummy = false;
     for (int k = 0; k < D; ++k) {
-      const float v = (k < d) ? (float)(packed_coord(seq, L, d, r, k, incr) * coord_scale) : 0.f;
+      const float v =
+          (k < d) ? (float)(packed_coord(seq, L, d, r, k, mode, true, dummy) * coord_scale) : 0.f;
       dst[2 * k + half] = v;
       nrm += (double)v * (double)v;
     }
-    dst[2 * D + half] = incr ? 0.f : (float)(-0.5 * nrm);
+    dst[2 * D + half] = nterm(mode, nrm, dummy);
     dst[2 * D + 2 + half] = 0.f;
   }
 }
@@ -69,7 +94,9 @@ struct Plan {
   bool ok = false;
   int D = 0, C = 8, sw = 0, segs = 0, npanel = 1, nhp = 0;
   bool linear = false;
-  int variant = 0;  // 0 rbf, 1 linear, 2 stationary kinds (matern*, rational quadratic)
+  bool nodiff = false;  // difference=False: the x role carries a dummy row 0
+  int variant = 0;  // 0 rbf, 1 linear, 2 stationary kinds (matern*, rational quadratic),
+                    // 3 rbf difference=False
 };
 
 bool stationary_kind(int kind) {
@@ -85,21 +112,25 @@ int next_pow2(int v) {
 
 constexpr size_t SMEM_LIMIT = 200 * 1024;
 
-int64_t pairs_of(int64_t lx) { return (lx + 1) / 2; }
+// x rows per sequence: L points, plus the dummy row 0 when difference=False
+int64_t pairs_of(int64_t lx, const Plan &pl) { return (lx + (pl.nodiff ? 1 : 0) + 1) / 2; }
 
 Plan plan_for(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   Plan pl;
   const int kind = c.static_spec.kind;
-  if (c.precision != SK_PREC_FP32 || !c.difference) return pl;
+  if (c.precision != SK_PREC_FP32) return pl;
   const bool stat = stationary_kind(kind);
   if (kind != SK_RBF && kind != SK_LINEAR && !stat) return pl;  // polynomial: float64 kernel
   if (stat && c.order != 1) return pl;  // stationary kinds: order-1 kernels only
+  pl.nodiff = !c.difference;
+  if (pl.nodiff && (stat || (kind == SK_RBF && c.order != 1))) return pl;  // not compiled
   if (!fast_orders_supported(c.n_levels, c.order)) return pl;
   // Normalised linear kernels of order > 1 are sensitive to the FP32
   // accumulation of the increment inner products (measured 1.6-2.1e-5 vs the
   // 1e-5 bar, also in a float64-recursion emulation): float64 kernel.
   if (kind == SK_LINEAR && c.order > 1 && c.normalization != SK_NORM_NONE) return pl;
-  if (d < 1 || d > 16 || lx < 2 || ly < 2) return pl;
+  const int64_t lmin = c.difference ? 2 : 1;  // difference=False: one point is one cell
+  if (d < 1 || d > 16 || lx < lmin || ly < lmin) return pl;
   pl.D = d <= 4 ? 4 : (d <= 8 ? 8 : 16);
   const int C = pl.C = columns_per_lane(c.order);
   if (ly <= 32 * C) {
@@ -113,13 +144,13 @@ Plan plan_for(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
       for (int m = 1; m < c.n_levels; ++m) nch += std::min(m + 1, (int)c.order) - 1;
     pl.nhp = (2 * nch + 3 + 3) / 4 * 4;
   }
-  const int64_t lx2 = pairs_of(lx);
+  const int64_t lx2 = pairs_of(lx, pl);
   if (lx2 < pl.sw) return pl;
   // + one pad record: the row prefetch may read one record past the last slot
   if (((size_t)NSLOT * lx2 + 1) * x_stride(pl.D) * sizeof(float) > SMEM_LIMIT) return pl;
   pl.segs = NWARPS * (32 / pl.sw);
   pl.linear = kind == SK_LINEAR;
-  pl.variant = pl.linear ? 1 : (stat ? 2 : 0);
+  pl.variant = pl.linear ? 1 : (stat ? 2 : (pl.nodiff ? 3 : 0));
   pl.ok = true;
   return pl;
 }
@@ -130,12 +161,12 @@ int lyp_of(const Plan &pl) { return pl.sw * pl.C * pl.npanel; }
 
 size_t carry_bytes(int64_t lx, const Plan &pl) {
   if (pl.npanel <= 1) return 0;
-  return align256((size_t)sm_count() * NWARPS * (RX_MULTI + 2) * pairs_of(lx) * pl.nhp *
+  return align256((size_t)sm_count() * NWARPS * (RX_MULTI + 2) * pairs_of(lx, pl) * pl.nhp *
                   sizeof(float));
 }
 
 size_t x_bytes(int64_t n, int64_t lx, const Plan &pl) {
-  return align256((size_t)n * pairs_of(lx) * x_stride(pl.D) * sizeof(float));
+  return align256((size_t)n * pairs_of(lx, pl) * x_stride(pl.D) * sizeof(float));
 }
 size_t y_bytes(int64_t n, const Plan &pl) {
   return align256((size_t)n * lyp_of(pl) * y_stride(pl.D) * sizeof(float));
@@ -187,9 +218,10 @@ int pack_roles(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t
   const size_t bx = x_bytes(nx, lx, pl), by = y_bytes(ny, pl);
   float *xsb = (float *)ws;
   float *ysb = (float *)((char *)ws + bx);
-  const int64_t lx2 = pairs_of(lx), lyp = lyp_of(pl);
+  const int64_t lx2 = pairs_of(lx, pl), lyp = lyp_of(pl);
   const double cs = coord_scale(c);
-  const int incr = pl.linear ? 1 : 0;  // linear: A = <dx, dy> directly
+  // packing mode (pack_x/pack_y): linear: A = <dx, dy> directly from increments
+  const int incr = pl.nodiff ? (pl.linear ? 3 : 2) : (pl.linear ? 1 : 0);
   if (nx > 0) {
     pack_x_kernel<<<pack_blocks(nx * lx2 * 2), 256, 0, st>>>(X, nx, lx, d, lx2, pl.D, cs, incr,
                                                              xsb);

@@ -249,8 +249,12 @@ __device__ __forceinline__ void double_difference(const float (&ga)[C], const fl
 // registers, the packed-FFMA2 point kernel of a row pair, and the double
 // difference (kernels.py:281) producing the increments of rows a and b.
 // ---------------------------------------------------------------------------
-template <int D, int C_, bool LINEAR>
+// KIND 0: rbf, double-differenced (kernels.py:281); 1: linear (the packed values
+// are increments, or points when difference=False: A is the point kernel
+// itself); 2: rbf with difference=False (A = G).
+template <int D, int C_, int KIND>
 struct PointStage {
+  static constexpr bool LINEAR = KIND == 1;
   static constexpr int C = C_;
   static constexpr int XP = x_stride(D);
   static constexpr int YP = y_stride(D);
@@ -319,7 +323,7 @@ struct PointStage {
 
   __device__ __forceinline__ void increments(float dla, float dlb, bool zero_left, float (&aa)[C],
                                              float (&ab)[C]) {
-    double_difference<C, LINEAR>(ga, gb, prevG, lastDa, lastDb, dla, dlb, zero_left, aa, ab);
+    double_difference<C, KIND != 0>(ga, gb, prevG, lastDa, lastDb, dla, dlb, zero_left, aa, ab);
   }
 };
 
@@ -828,13 +832,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) gram_kernel(const Params P) {
 //  y role: [N][Lp][D+4], point p = min(p, L-1), n-term at column D.
 //  x role: [N][Lp2][2D+4] row pairs, rows (2t, 2t+1) interleaved per
 //          channel, n-terms at 2D, 2D+1; rows beyond L repeat the last point.
-//  incr = 1 (linear kind): each point is replaced by the increment ending
-//  there, x_p - x_{p-1} (0 for p = 0 and beyond L), computed in float64.
+//  mode (pack_mode): 0 points; 1 increments x_p - x_{p-1} (0 for p = 0 and
+//  beyond L, formed in float64; linear kind); 2/3 difference=False (rbf /
+//  linear): the x role gets a dummy row 0 (the discarded first row of every
+//  pair), and rows/columns beyond L are dummies whose point kernel is 0 (rbf:
+//  n-term -1e30, so exp2 underflows to 0; linear: zero coordinates).
 __global__ void pack_y_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
-                              int64_t Lp, int D, double coord_scale, int incr,
+                              int64_t Lp, int D, double coord_scale, int mode,
                               float *__restrict__ out);
 __global__ void pack_x_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
-                              int64_t Lp2, int D, double coord_scale, int incr,
+                              int64_t Lp2, int D, double coord_scale, int mode,
                               float *__restrict__ out);
 
 int launch_d4(const Params &, int M, int order, int variant, size_t smem, cudaStream_t st);
@@ -865,9 +872,11 @@ int launch_kernel(const Params &P, size_t smem, cudaStream_t st) {
   return SK_OK;
 }
 
-// variant: 0 rbf, 1 linear, 2 stationary kinds (StatPointStage, order 1 only)
-template <int D, bool LIN>
+// variant: 0 rbf, 1 linear, 2 stationary kinds (StatPointStage, order 1 only),
+// 3 rbf with difference=False (order 1 only)
+template <int D, int LIN>
 int launch_impl_lin(const Params &P, int M, int order, size_t smem, cudaStream_t st) {
+  if (LIN == 2 && order != 1) return fail(SK_ERR_UNSUPPORTED, "fast path: order not compiled");
   if (order == 1) {
     switch (M) {
       case 1: return launch_kernel<LaneState1<PointStage<D, 8, LIN>, 1>>(P, smem, st);
@@ -880,7 +889,7 @@ int launch_impl_lin(const Params &P, int M, int order, size_t smem, cudaStream_t
       case 8: return launch_kernel<LaneState1<PointStage<D, 8, LIN>, 8>>(P, smem, st);
       default: break;
     }
-  } else if (order == M) {
+  } else if (order == M && LIN != 2) {
     switch (M) {
       case 2: return launch_kernel<LaneStateG<PointStage<D, 4, LIN>, 2, 2>>(P, smem, st);
       case 3: return launch_kernel<LaneStateG<PointStage<D, 4, LIN>, 3, 3>>(P, smem, st);
@@ -914,8 +923,9 @@ int launch_impl_stat(const Params &P, int M, int order, size_t smem, cudaStream_
 template <int D>
 int launch_impl(const Params &P, int M, int order, int variant, size_t smem, cudaStream_t st) {
   if (variant == 2) return launch_impl_stat<D>(P, M, order, smem, st);
-  return variant == 1 ? launch_impl_lin<D, true>(P, M, order, smem, st)
-                      : launch_impl_lin<D, false>(P, M, order, smem, st);
+  if (variant == 3) return launch_impl_lin<D, 2>(P, M, order, smem, st);
+  return variant == 1 ? launch_impl_lin<D, 1>(P, M, order, smem, st)
+                      : launch_impl_lin<D, 0>(P, M, order, smem, st);
 }
 
 }  // namespace fast

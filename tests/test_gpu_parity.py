@@ -558,3 +558,30 @@ def test_stationary_kind_multi_panel():
     R = O.gram(X, Y, sp=O.static_params("matern32", bandwidth=1.2), M=4, p=1,
                normalization="levelwise")
     assert _scaled_err(sig_kernel_gram(X, Y, cfg=cfg), R) <= TOL_NORM
+
+
+@pytest.mark.parametrize("kind", ["rbf", "linear"])
+def test_difference_false_fused(kind):
+    """difference=False (kernels.py:275-276): A = G on the L x L' grid, fused FP32."""
+    X = gen_brownian(6, 40, 3, SeedStream(61)).data
+    Y = gen_brownian(5, 33, 3, SeedStream(62)).data
+    sp = O.static_params(kind)
+    orders = (1, 3) if kind == "linear" else (1,)
+    for p in orders:
+        for norm, tol in (("none", TOL_RAW), ("levelwise", TOL_NORM)):
+            if kind == "linear" and p > 1 and norm != "none":
+                continue
+            cfg = KernelConfig(static=StaticKernelSpec(kind=kind), n_levels=3, order=p,
+                               difference=False, normalization=norm)
+            assert uses_fast_path(40, 33, 3, cfg)
+            R = O.gram(X, Y, sp=sp, M=3, p=p, difference=False, normalization=norm)
+            assert _scaled_err(sig_kernel_gram(X, Y, cfg=cfg), R) <= tol, (kind, p, norm)
+            assert _scaled_err(sig_kernel_gram(Y, X, cfg=cfg), R.T) <= tol, (kind, p, norm)
+    cfg = KernelConfig(static=StaticKernelSpec(kind=kind), n_levels=3, difference=False,
+                       normalization="levelwise")
+    K = sig_kernel_gram(X, cfg=cfg)
+    assert np.array_equal(K, K.T) and np.array_equal(np.diag(K), np.ones(6))
+    one = np.random.default_rng(3).standard_normal((2, 1, 3))  # one point = one raw cell
+    R1 = O.gram(one, one, sp=sp, M=3, p=1, difference=False)
+    cfg = KernelConfig(static=StaticKernelSpec(kind=kind), n_levels=3, difference=False)
+    assert _scaled_err(sig_kernel_gram(one, one, cfg=cfg), R1) <= TOL_RAW
