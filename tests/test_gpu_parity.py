@@ -585,3 +585,41 @@ def test_difference_false_fused(kind):
     R1 = O.gram(one, one, sp=sp, M=3, p=1, difference=False)
     cfg = KernelConfig(static=StaticKernelSpec(kind=kind), n_levels=3, difference=False)
     assert _scaled_err(sig_kernel_gram(one, one, cfg=cfg), R1) <= TOL_RAW
+
+
+# ---------------------------------------------------------------------------
+# full BASELINE sizes: the whole Gram on the device, checked through its
+# prefix-stable golden block (gen_brownian is prefix-stable: the first k
+# sequences of the full batch are the golden inputs) and size-independent
+# properties
+# ---------------------------------------------------------------------------
+
+FULL = {  # name: (N, L, d, golden case)
+    "c3": (8192, 256, 16, "bench_c3"),
+    "c2": (1024, 128, 8, "bench_c2"),
+    "c2n": (1024, 128, 8, "bench_c2n"),
+    "c4": (4096, 128, 128, "bench_c4"),
+    "c5": (512, 2048, 4, "bench_c5"),
+    "c5n": (512, 2048, 4, "bench_c5n"),
+}
+
+
+@pytest.mark.parametrize("name", sorted(FULL))
+def test_full_size_baseline_configs(gram_cases, name):
+    N, L, d, golden = FULL[name]
+    _, Xg, Yg, c, K_ref = gram_cases.get(golden)
+    k = Xg.shape[0]
+    X = torch.from_numpy(gen_brownian(N, L, d, SeedStream(1)).data).cuda()
+    Y = torch.from_numpy(gen_brownian(N, L, d, SeedStream(2)).data).cuda()
+    assert np.array_equal(X[:k].cpu().numpy(), Xg) and np.array_equal(Y[:k].cpu().numpy(), Yg)
+    cfg = pkg_config(c)
+    K = sig_kernel_gram(X, Y, cfg=cfg)
+    assert K.shape == (N, N) and bool(torch.isfinite(K).all())
+    tol = TOL_RAW if c["normalization"] == "none" else TOL_NORM
+    assert _rel(K[:k, :k].cpu().numpy(), K_ref) <= tol
+    if c["normalization"] != "none":
+        assert float(K.abs().max()) <= 1.0 + 1e-6
+    # row blocks of the full Gram are the Gram of the row blocks (no cross-row state)
+    rows = torch.arange(N - 3, N, device="cuda")
+    Kb = sig_kernel_gram(X[rows], Y, cfg=cfg)
+    assert torch.equal(Kb, K[rows])
