@@ -849,9 +849,9 @@ int launch_d8(const Params &, int M, int order, int variant, size_t smem, cudaSt
 int launch_d16(const Params &, int M, int order, int variant, size_t smem, cudaStream_t st);
 
 // Compiled (n_levels, order) combinations: order 1 with n_levels 1..8, and
-// the geometric kernel order = n_levels for n_levels 2..5.
+// every order 2 <= p <= n_levels for n_levels 2..5 (p = n_levels: geometric).
 __host__ __device__ constexpr bool fast_orders_supported(int M, int order) {
-  return (order == 1 && M >= 1 && M <= 8) || (order == M && M >= 2 && M <= 5);
+  return (order == 1 && M >= 1 && M <= 8) || (order >= 2 && order <= M && M <= 5);
 }
 __host__ __device__ constexpr int columns_per_lane(int order) { return order == 1 ? 8 : 4; }
 
@@ -889,14 +889,12 @@ int launch_impl_lin(const Params &P, int M, int order, size_t smem, cudaStream_t
       case 8: return launch_kernel<LaneState1<PointStage<D, 8, LIN>, 8>>(P, smem, st);
       default: break;
     }
-  } else if (order == M && LIN != 2) {
-    switch (M) {
-      case 2: return launch_kernel<LaneStateG<PointStage<D, 4, LIN>, 2, 2>>(P, smem, st);
-      case 3: return launch_kernel<LaneStateG<PointStage<D, 4, LIN>, 3, 3>>(P, smem, st);
-      case 4: return launch_kernel<LaneStateG<PointStage<D, 4, LIN>, 4, 4>>(P, smem, st);
-      case 5: return launch_kernel<LaneStateG<PointStage<D, 4, LIN>, 5, 5>>(P, smem, st);
-      default: break;
-    }
+  } else if (LIN != 2) {
+#define SK_G(MM, PP) \
+  if (M == MM && order == PP) return launch_kernel<LaneStateG<PointStage<D, 4, LIN>, MM, PP>>(P, smem, st);
+    SK_G(2, 2) SK_G(3, 2) SK_G(3, 3) SK_G(4, 2) SK_G(4, 3) SK_G(4, 4)
+    SK_G(5, 2) SK_G(5, 3) SK_G(5, 4) SK_G(5, 5)
+#undef SK_G
   }
   return fail(SK_ERR_UNSUPPORTED, "fast path: (n_levels, order) not compiled");
 }

@@ -46,7 +46,9 @@ def test_fast_path_selection():
     geo = _native.config_struct(KernelConfig(n_levels=5, order=5))
     assert lib.sk_fast_path(128, 128, 8, geo) == 1          # geometric p = M (c2)
     mid = _native.config_struct(KernelConfig(n_levels=5, order=3))
-    assert lib.sk_fast_path(128, 128, 8, mid) == 0          # 1 < p < M: float64 kernel
+    assert lib.sk_fast_path(128, 128, 8, mid) == 1          # 1 < p < M: fused general order
+    big = _native.config_struct(KernelConfig(n_levels=6, order=3))
+    assert lib.sk_fast_path(128, 128, 8, big) == 0          # p > 1 beyond n_levels 5: float64
     lgeo = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="linear"), n_levels=4,
                                               order=4, normalization="levelwise"))
     assert lib.sk_fast_path(64, 64, 4, lgeo) == 0           # normalised linear p > 1: float64

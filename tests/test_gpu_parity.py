@@ -623,3 +623,17 @@ def test_full_size_baseline_configs(gram_cases, name):
     rows = torch.arange(N - 3, N, device="cuda")
     Kb = sig_kernel_gram(X[rows], Y, cfg=cfg)
     assert torch.equal(Kb, K[rows])
+
+
+@pytest.mark.parametrize("M,p", [(3, 2), (4, 2), (4, 3), (5, 2), (5, 3), (5, 4)])
+def test_intermediate_orders_fused(M, p):
+    """1 < p < M (test_kernels.py:143-150 sweeps p = 1..4 at M = 4) on the fused kernel."""
+    X = gen_brownian(6, 50, 4, SeedStream(71)).data
+    Y = gen_brownian(5, 37, 4, SeedStream(72)).data
+    for kind, norm, tol in (("rbf", "none", TOL_RAW), ("rbf", "levelwise", TOL_NORM),
+                            ("linear", "none", TOL_RAW)):
+        cfg = KernelConfig(static=StaticKernelSpec(kind=kind), n_levels=M, order=p,
+                           normalization=norm)
+        assert uses_fast_path(50, 37, 4, cfg)
+        R = O.gram(X, Y, sp=O.static_params(kind), M=M, p=p, normalization=norm)
+        assert _scaled_err(sig_kernel_gram(X, Y, cfg=cfg), R) <= tol, (kind, norm)
