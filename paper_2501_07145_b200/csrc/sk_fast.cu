@@ -88,7 +88,10 @@ __global__ void pack_x_kernel(const double *__restrict__ X, int64_t n, int64_t L
 
 namespace {
 
-constexpr int RX_MULTI = 8;  // x sequences per tile when the carry buffer is in use
+#ifndef SK_RX_MULTI
+#define SK_RX_MULTI 8
+#endif
+constexpr int RX_MULTI = SK_RX_MULTI;  // x sequences per tile when the carry buffer is in use
 
 struct Plan {
   bool ok = false;
