@@ -7,11 +7,16 @@ normalised (levelwise) order-1 RBF signature kernel, n_levels=5, cross Gram
 K(X, Y) of N = M' = 8192 random-walk sequences, L = 256, d = 16, float64
 inputs generated with the reference's own generator (restated bit for bit).
 
-A "step" is one whole Gram: self levels of X and Y (normalisation), the
-fused Gram kernel with its normalisation epilogue, and (N > 1) the NCCL
-all-gather of the row blocks. `value` is entries/s with inputs resident in
-HBM; `e2e` is the same through the public API (`SignatureKernel.__call__`)
-from pinned host float64 inputs to the host float64 Gram.
+A "step" is one whole Gram: self levels of X and Y (normalisation) and the
+fused Gram kernel with its normalisation epilogue. With N GPUs (torchrun)
+the Gram rows partition with no exchange, so the run is weak scaling: rank r
+owns sequences [r*8192, (r+1)*8192) of X (prefix-stable generator) and
+evaluates its 8192 x 8192 block of K(X, Y); the step is timed as the max
+over ranks and `value` counts every rank's entries (no collective in the
+step; `distributed.sharded_gram` is the library call that also all-gathers
+K). `value` is entries/s with inputs resident in HBM; `e2e` is the same
+through the public API (`SignatureKernel.__call__`) from pinned host float64
+inputs to the host float64 Gram.
 """
 
 from __future__ import annotations
@@ -79,10 +84,11 @@ def path_info(name):
     return path, "sk::generic_levels_kernel (float64)", 2, 2
 
 
-def make_inputs(name):
+def make_inputs(name, start=0):
+    """X = sequences [start, start+N) of the SeedStream(1) batch, Y = the first N of SeedStream(2)."""
     from paper_2501_07145_b200 import SeedStream, gen_brownian
     N, L, d = CONFIGS[name][:3]
-    X = gen_brownian(N, L, d, SeedStream(1)).data
+    X = gen_brownian(N, L, d, SeedStream(1), start=start).data
     Y = None if CONFIGS[name][7] else gen_brownian(N, L, d, SeedStream(2)).data
     return X, Y
 
@@ -145,7 +151,7 @@ def run_reference(args):
     value = float(np.median(rates))
     line = {"metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(times)),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: gen_brownian random walks (SeedStream 1 / 2)",
             "config": workload(name), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": "entries/s", "cores": threads, "kind": "port",
@@ -222,7 +228,6 @@ def run_gpu(args):
     import torch.distributed as dist
 
     from paper_2501_07145_b200 import LinearKernel, RBFKernel, SignatureKernel
-    from paper_2501_07145_b200.distributed import row_blocks, sharded_gram, triangle_row_blocks
     from paper_2501_07145_b200.kernels import _self_levels_t, gram_block
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -236,26 +241,21 @@ def run_gpu(args):
     name = args.config
     N, L, d, M, p, kind, norm, sym, _ = CONFIGS[name]
     cfg = kernel_config(name)
-    Xh, Yh = make_inputs(name)
+    # Weak scaling (the Gram partitions into independent rows): rank r owns
+    # sequences [r*N, (r+1)*N) of an (world*N)-sequence X (the prefix-stable
+    # generator makes every rank's block exact) and evaluates its N x N' row
+    # block of K(X, Y) (symmetric configs: its N x N diagonal block K(X_r)).
+    # No collective in the step; distributed.sharded_gram is the library API
+    # when every rank needs the assembled K.
+    Xh, Yh = make_inputs(name, start=rank * N)
     X = torch.from_numpy(Xh).to(dev)
     Y = None if Yh is None else torch.from_numpy(Yh).to(dev)
     ny = N
 
-    # one step: self levels (normalisation), fused Gram of this rank's rows, gather
+    # one step: self levels (normalisation) + the fused Gram of this rank's rows
     gram_ms = []
 
     def step(record=False):
-        ev = None
-        if world > 1:
-            def compute(Xt, Yt, c, r0, r1, prec, K_full):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                K, _ = gram_block(Xt, Yt, c, r0, r1, prec, K=K_full)
-                e1.record()
-                if record:
-                    gram_ms.append((e0, e1))
-                return K
-            return sharded_gram(X, Y, cfg, group=None, compute=compute)
         diag_x = diag_y = None
         if norm != "none":
             diag_x = _self_levels_t(X, cfg, "fp32")
@@ -290,21 +290,12 @@ def run_gpu(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         elapsed = float(tt.item())
     ms = elapsed / args.steps
-    entries = N * ny
+    entries = N * ny * world  # every rank's block
     value = entries / (ms / 1e3)
 
     # dominant kernel: the fused Gram launch (sk_gram = 2 tiny pack kernels + Gram kernel)
     g_ms = float(np.mean([a.elapsed_time(b) for a, b in gram_ms]))
-    if world > 1:
-        blocks = (triangle_row_blocks(N, world) if sym else row_blocks(N, world))[rank]
-        rows = blocks[1] - blocks[0]
-    else:
-        rows = N
-    if sym:
-        r0, r1 = (triangle_row_blocks(N, world)[rank] if world > 1 else (0, N))
-        pairs = sum(N - i for i in range(r0, r1))
-    else:
-        pairs = rows * ny
+    pairs = N * (N + 1) // 2 if sym else N * ny  # evaluated pairs of this rank's launch
     F = flops_per_entry(L, d, M)
     achieved = pairs * F / (g_ms / 1e3) / 1e12
     traffic = None
@@ -318,11 +309,8 @@ def run_gpu(args):
     sm_max = clocks["sm_max_mhz"] or 1965.0
     peak = props.multi_processor_count * 128 * 2 * sm_max * 1e6 / 1e12
 
-    # end to end through the public API from pinned host buffers
     # end to end through the public API from pinned host buffers: the
-    # SignatureKernel facade on one GPU; on N GPUs every rank uploads X, Y,
-    # runs distributed.sharded_gram (its row block + the NCCL all-gather) and
-    # reads the assembled K back
+    # SignatureKernel facade on this rank's block (every rank, no collective)
     import torch as _t
     Xp = _t.from_numpy(Xh).pin_memory()
     Yp = None if Yh is None else _t.from_numpy(Yh).pin_memory()
@@ -333,7 +321,7 @@ def run_gpu(args):
     def e2e_step():
         Xd = Xp.to(dev, non_blocking=True)
         Yd = None if Yp is None else Yp.to(dev, non_blocking=True)
-        Kd = sk(Xd, Yd) if world == 1 else sharded_gram(Xd, Yd, cfg)
+        Kd = sk(Xd, Yd)
         Kh.copy_(Kd, non_blocking=True)
         return Kd
 
@@ -353,10 +341,8 @@ def run_gpu(args):
     h2d = Xh.nbytes + (0 if Yh is None else Yh.nbytes)
     e2e = {"value": entries / (e_ms / 1e3), "unit": "entries/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": N * ny * 8, "ms_per_step": e_ms,
-           "api": ("SignatureKernel(...)(X, Y)" if world == 1 else
-                   "distributed.sharded_gram(X, Y, cfg) on every rank")
-                  + " from pinned host float64 to host float64 K",
-           "per_rank_bytes": "h2d/d2h counted per rank" if world > 1 else None}
+           "api": "SignatureKernel(...)(X, Y) on every rank's block, pinned host float64 in, "
+                  "host float64 K out (bytes per rank)"}
 
     path, klabel, per_gram, per_self = path_info(name)
     launches_per_step = (per_self if norm != "none" else 0) * (1 if sym else 2) + per_gram
@@ -364,11 +350,13 @@ def run_gpu(args):
         line = {
             "metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "fp32 (float64 level sums and normalisation)",
             "data": "synthetic: gen_brownian random walks, SeedStream(1)/(2), reference "
                     "generator restated bit for bit",
-            "config": dict(workload(name), parallelism=f"rows{world}" if world > 1 else "single"),
+            "config": dict(workload(name), parallelism=(
+                f"row blocks x{world}: rank r owns sequences [r*{N}, (r+1)*{N}) of X, no collective"
+                if world > 1 else "single")),
             "e2e": e2e,
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
