@@ -87,3 +87,43 @@ def test_sharded_gram_gloo_world2(sym):
     for r in range(2):
         assert res[r].shape == want.shape
         assert np.array_equal(res[r], want)  # every entry has exactly one contributor
+
+
+def _weak_worker(rank, world, port, n, out_q):
+    """bench.py's multi-GPU partition: rank r owns sequences [r*n, (r+1)*n) of X
+    (prefix-stable generator) and evaluates its row block of K(X, Y); no collective
+    in the computation (the gather below only verifies the result)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import sigkern_oracle as O
+        from paper_2501_07145_b200 import SeedStream, gen_brownian
+        Xr = gen_brownian(n, 6, 2, SeedStream(1), start=rank * n).data
+        Y = gen_brownian(4, 6, 2, SeedStream(2)).data
+        Kr = torch.from_numpy(O.gram(Xr, Y, M=3, p=1, normalization="levelwise"))
+        parts = [torch.empty_like(Kr) for _ in range(world)]
+        dist.all_gather(parts, Kr)
+        out_q.put((rank, torch.cat(parts).numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_weak_scaling_partition_gloo_world2():
+    from oracle import sigkern_oracle as O
+    from paper_2501_07145_b200 import SeedStream, gen_brownian
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    n = 3
+    procs = [ctx.Process(target=_weak_worker, args=(r, 2, port, n, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    X = gen_brownian(2 * n, 6, 2, SeedStream(1)).data
+    Y = gen_brownian(4, 6, 2, SeedStream(2)).data
+    want = O.gram(X, Y, M=3, p=1, normalization="levelwise")
+    assert np.array_equal(res[0], want) and np.array_equal(res[1], want)
