@@ -189,6 +189,62 @@ SK_API int sk_pde_self(const double *X, int64_t n, int64_t l, int64_t d,
                 const sk_static_spec *spec, int32_t difference, double *out,
                 void *workspace, size_t workspace_bytes, void *stream);
 
+/*
+ * rfsf_exact_gram (features.py:446-475): exact Gram of a fitted rfsf_full
+ * random-feature map via its finite-rank lift (_lifted_level_grams,
+ * features.py:397-424). Level m of the dual DP uses the static kernel
+ * <phi_m(x), phi_m(y)> of slot m's feature map, so the DP consumes one
+ * increment matrix per level (kernels.py:129-141). Float64 throughout.
+ */
+enum sk_feature_kind { SK_FEAT_RFF = 0, SK_FEAT_RFF1D = 1, SK_FEAT_NYSTROEM = 2 };
+
+/* A fitted static feature map (StaticFeatureState, static/features.py:56-66);
+ * every pointer is device memory. */
+typedef struct sk_feature_map {
+  int32_t kind;            /* sk_feature_kind */
+  int32_t reserved;        /* must be 0 */
+  int64_t n_components;    /* D */
+  int64_t out_dim;         /* 2D (rff), D (rff1d), kept eigenvalues (nystroem) */
+  const double *weights;   /* (d, D) frequencies: rff, rff1d */
+  const double *phases;    /* (D,) offsets: rff1d */
+  const double *landmarks; /* (D, d) landmark rows: nystroem */
+  const double *whiten;    /* (D, out_dim): nystroem */
+  sk_static_spec base;     /* nystroem base kernel */
+} sk_feature_map;
+
+/*
+ * transform_static_features (static/features.py:102-124): X is (npts, d);
+ * feature row p is written at out[p*ld_out + 0 .. out_dim). The nystroem map
+ * needs sk_static_features_workspace_bytes of workspace (0 for rff kinds).
+ */
+SK_API size_t sk_static_features_workspace_bytes(const sk_feature_map *map, int64_t npts);
+SK_API int sk_static_features(const sk_feature_map *map, const double *X, int64_t npts,
+                       int64_t d, double *out, int64_t ld_out,
+                       void *workspace, size_t workspace_bytes, void *stream);
+
+/*
+ * Lifted level Grams. UX (nx, lx, width) / UY (ny, ly, width) hold every
+ * slot's features concatenated along the last axis; slot m (level m+1) owns
+ * channels [slot_offsets[m], slot_offsets[m+1]), m = 0..n_levels-1
+ * (slot_offsets is HOST memory, n_levels+1 entries). `order` is the effective
+ * order; K / levels / rows / symmetric / diag as in sk_gram, diag from
+ * sk_lifted_self_levels (_lifted_self_levels, features.py:427-443) when
+ * normalization is SK_NORM_LEVELWISE.
+ */
+SK_API size_t sk_lifted_workspace_bytes(int64_t npairs, int64_t ly, int32_t n_levels,
+                                 int32_t order, int32_t difference);
+SK_API int sk_lifted_gram(const double *UX, int64_t nx, int64_t lx, const double *UY,
+                   int64_t ny, int64_t ly, int64_t width, const int64_t *slot_offsets,
+                   int32_t n_levels, int32_t order, int32_t difference,
+                   int32_t normalization, int32_t symmetric, int64_t row_begin,
+                   int64_t row_end, const double *diag_x, const double *diag_y, double *K,
+                   int64_t ldk, double *levels, void *workspace, size_t workspace_bytes,
+                   void *stream);
+SK_API int sk_lifted_self_levels(const double *UX, int64_t n, int64_t l, int64_t width,
+                          const int64_t *slot_offsets, int32_t n_levels, int32_t order,
+                          int32_t difference, double *out, void *workspace,
+                          size_t workspace_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -381,5 +381,76 @@ def gram(X, Y=None, *, sp=None, M=5, p=1, difference=True, normalization="none",
     return normalize_global(lv.sum(axis=-1), dx.sum(axis=-1), dy.sum(axis=-1))
 
 
+# --- rfsf_exact_gram (features.py:397-475) -----------------------------------
+
+def static_features(slot, X):
+    """transform_static_features (static/features.py:102-124) of a fitted slot,
+    given as a dict: kind ("rff"/"rff1d"/"nystroem"), n_components, weights,
+    phases, landmarks, whiten, base (static_params of the nystroem base kernel)."""
+    X = np.asarray(X, dtype=np.float64)
+    D = int(slot["n_components"])
+    if slot["kind"] == "rff":
+        P = X @ slot["weights"]
+        s = 1.0 / math.sqrt(D)
+        return np.concatenate([s * np.cos(P), s * np.sin(P)], axis=-1)
+    if slot["kind"] == "rff1d":
+        return math.sqrt(2.0 / D) * np.cos(X @ slot["weights"] + slot["phases"])
+    lead = X.shape[:-1]
+    K = point_gram(slot["base"], X.reshape(-1, X.shape[-1]), slot["landmarks"])
+    return (K @ slot["whiten"]).reshape(*lead, slot["whiten"].shape[1])
+
+
+def lifted_levels(slots, Xa, Xb, M, p, difference=True):
+    """_lifted_level_grams (features.py:397-424): level m's increments come from
+    slot m's feature inner products. -> (Na, Nb, M+1)."""
+    Na, La = Xa.shape[:2]
+    Nb, Lb = Xb.shape[:2]
+    if M == 0:
+        return np.ones((Na, Nb, 1))
+    mats = []
+    for slot in slots:
+        Ux = static_features(slot, Xa)
+        Uy = static_features(slot, Xb)
+        G = (Ux.reshape(Na * La, -1) @ Uy.reshape(Nb * Lb, -1).T).reshape(
+            Na, La, Nb, Lb).transpose(0, 2, 1, 3)
+        mats.append(G[..., 1:, 1:] - G[..., :-1, 1:] - G[..., 1:, :-1] + G[..., :-1, :-1]
+                    if difference else G)
+    return levels_dp(mats, M, p)
+
+
+def lifted_self_levels(slots, Xa, M, p, difference=True):
+    """_lifted_self_levels (features.py:427-443). -> (N, M+1)."""
+    if M == 0:
+        return np.ones((Xa.shape[0], 1))
+    mats = []
+    for slot in slots:
+        U = static_features(slot, Xa)
+        G = U @ U.transpose(0, 2, 1)
+        mats.append(G[..., 1:, 1:] - G[..., :-1, 1:] - G[..., 1:, :-1] + G[..., :-1, :-1]
+                    if difference else G)
+    return levels_dp(mats, M, p)
+
+
+def rfsf_exact_gram(slots, X, Y=None, M=None, p=1, difference=True, normalize=False):
+    """rfsf_exact_gram (features.py:446-475) from fitted slot dicts."""
+    M = len(slots) if M is None else M
+    Xa = np.asarray(X, dtype=np.float64)
+    sym = Y is None
+    Xb = Xa if sym else np.asarray(Y, dtype=np.float64)
+    levels = lifted_levels(slots, Xa, Xb, M, p, difference)
+    if not normalize:
+        K = levels.sum(axis=-1)
+    else:
+        if sym:
+            dx = dy = np.einsum("iim->im", levels).copy()
+        else:
+            dx = lifted_self_levels(slots, Xa, M, p, difference)
+            dy = lifted_self_levels(slots, Xb, M, p, difference)
+        K = normalize_levelwise(levels, dx, dy)
+    if sym:
+        K = np.triu(K) + np.triu(K, 1).T
+    return K
+
+
 def host_threads() -> int:
     return len(os.sched_getaffinity(0))

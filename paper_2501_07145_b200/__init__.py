@@ -9,6 +9,7 @@ from .errors import ConfigError, NativeError, NumericError, SigkernError
 from .facade import (LinearKernel, Matern12Kernel, Matern32Kernel, Matern52Kernel,
                      PolynomialKernel, RationalQuadraticKernel, RBFKernel, SignatureKernel,
                      StaticKernel)
+from .features import SigFeatureConfig, fit_sig_features, rfsf_exact_gram
 from .kernels import (increment_tensor, self_levels, sig_kernel_dp, sig_kernel_gram,
                       sig_levels_dp, sig_pde_kernel, uses_fast_path)
 from .sequences import SeedStream, SequenceBatch, gen_brownian
@@ -24,5 +25,5 @@ __all__ = [
     "Matern32Kernel", "Matern52Kernel", "RationalQuadraticKernel", "SignatureKernel",
     "increment_tensor", "self_levels", "sig_kernel_dp", "sig_kernel_gram", "sig_levels_dp", "sig_pde_kernel",
     "uses_fast_path", "median_heuristic", "SeedStream", "SequenceBatch", "gen_brownian", "ResourceCounters",
-    "__version__",
+    "SigFeatureConfig", "fit_sig_features", "rfsf_exact_gram", "__version__",
 ]

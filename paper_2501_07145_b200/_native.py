@@ -25,7 +25,8 @@ PREC_CODES = {"fp32": 0, "fp64": 1}
 EXPORTS = ("sk_abi_version", "sk_last_error", "sk_workspace_bytes", "sk_fast_path",
            "sk_self_levels", "sk_gram", "sk_levels_dp_workspace_bytes", "sk_levels_dp",
            "sk_increment_tensor", "sk_pairwise_dist", "sk_pde_workspace_bytes", "sk_pde_gram",
-           "sk_pde_self")
+           "sk_pde_self", "sk_static_features_workspace_bytes", "sk_static_features",
+           "sk_lifted_workspace_bytes", "sk_lifted_gram", "sk_lifted_self_levels")
 
 
 class SkStaticSpec(ctypes.Structure):
@@ -39,6 +40,14 @@ class SkKernelConfig(ctypes.Structure):
                 ("order", ctypes.c_int32), ("difference", ctypes.c_int32),
                 ("normalization", ctypes.c_int32), ("precision", ctypes.c_int32),
                 ("reserved", ctypes.c_int32)]
+
+
+class SkFeatureMap(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("n_components", ctypes.c_int64), ("out_dim", ctypes.c_int64),
+                ("weights", ctypes.c_void_p), ("phases", ctypes.c_void_p),
+                ("landmarks", ctypes.c_void_p), ("whiten", ctypes.c_void_p),
+                ("base", SkStaticSpec)]
 
 
 _lock = threading.Lock()
@@ -75,6 +84,19 @@ def _declare(lib):
     lib.sk_pde_self.argtypes = [P, I64, I64, I64, SPEC, I32, P, P, SZ, P]
     lib.sk_pairwise_dist.restype = ctypes.c_int
     lib.sk_pairwise_dist.argtypes = [P, I64, I64, P, P]
+    FMAP = ctypes.POINTER(SkFeatureMap)
+    OFFS = ctypes.POINTER(ctypes.c_int64)
+    lib.sk_static_features_workspace_bytes.restype = SZ
+    lib.sk_static_features_workspace_bytes.argtypes = [FMAP, I64]
+    lib.sk_static_features.restype = ctypes.c_int
+    lib.sk_static_features.argtypes = [FMAP, P, I64, I64, P, I64, P, SZ, P]
+    lib.sk_lifted_workspace_bytes.restype = SZ
+    lib.sk_lifted_workspace_bytes.argtypes = [I64, I64, I32, I32, I32]
+    lib.sk_lifted_gram.restype = ctypes.c_int
+    lib.sk_lifted_gram.argtypes = [P, I64, I64, P, I64, I64, I64, OFFS, I32, I32, I32, I32, I32,
+                                   I64, I64, P, P, P, I64, P, P, SZ, P]
+    lib.sk_lifted_self_levels.restype = ctypes.c_int
+    lib.sk_lifted_self_levels.argtypes = [P, I64, I64, I64, OFFS, I32, I32, I32, P, P, SZ, P]
     lib.sk_increment_tensor.restype = ctypes.c_int
     lib.sk_increment_tensor.argtypes = [P, I64, I64, P, I64, I64, I64, I32,
                                         ctypes.POINTER(SkStaticSpec), I32, P, P]

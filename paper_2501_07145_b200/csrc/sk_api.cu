@@ -246,4 +246,93 @@ int sk_pde_self(const double *X, int64_t n, int64_t l, int64_t d, const sk_stati
                   (cudaStream_t)stream);
 }
 
+size_t sk_static_features_workspace_bytes(const sk_feature_map *map, int64_t npts) {
+  return map ? static_features_workspace_bytes(*map, npts) : 0;
+}
+
+int sk_static_features(const sk_feature_map *map, const double *X, int64_t npts, int64_t d,
+                       double *out, int64_t ld_out, void *workspace, size_t workspace_bytes,
+                       void *stream) {
+  clear_error();
+  if (!map) return fail(SK_ERR_INVALID, "feature map is NULL");
+  if (map->kind < SK_FEAT_RFF || map->kind > SK_FEAT_NYSTROEM)
+    return fail(SK_ERR_INVALID, "unknown feature kind " + std::to_string(map->kind));
+  if (map->reserved != 0) return fail(SK_ERR_INVALID, "reserved must be 0");
+  if (map->n_components < 1) return fail(SK_ERR_INVALID, "n_components must be a positive integer");
+  const int64_t want = map->kind == SK_FEAT_RFF ? 2 * map->n_components
+                       : map->kind == SK_FEAT_RFF1D ? map->n_components : -1;
+  if (want >= 0 && map->out_dim != want)
+    return fail(SK_ERR_INVALID, "out_dim does not match the feature kind");
+  if (map->out_dim < 0 || map->out_dim > std::max<int64_t>(map->n_components, want))
+    return fail(SK_ERR_INVALID, "out_dim outside [0, n_components]");
+  if (npts < 0 || d < 1) return fail(SK_ERR_INVALID, "expected (npts, d) points with d >= 1");
+  if (ld_out < map->out_dim) return fail(SK_ERR_INVALID, "ld_out < out_dim");
+  if (npts == 0) return SK_OK;
+  if (!X || !out) return fail(SK_ERR_INVALID, "NULL pointer");
+  if (map->kind == SK_FEAT_NYSTROEM) {
+    int rc;
+    if ((rc = check_static(&map->base))) return rc;
+    if (!map->landmarks || (map->out_dim > 0 && !map->whiten))
+      return fail(SK_ERR_INVALID, "nystroem map needs landmarks and whiten");
+  } else if (!map->weights || (map->kind == SK_FEAT_RFF1D && !map->phases)) {
+    return fail(SK_ERR_INVALID, "rff map needs weights (and phases for rff1d)");
+  }
+  return static_features(*map, X, npts, d, out, ld_out, workspace, workspace_bytes,
+                         (cudaStream_t)stream);
+}
+
+size_t sk_lifted_workspace_bytes(int64_t npairs, int64_t ly, int32_t n_levels, int32_t order,
+                                 int32_t difference) {
+  return lifted_workspace_bytes(npairs, ly, n_levels, order, difference);
+}
+
+int sk_lifted_gram(const double *UX, int64_t nx, int64_t lx, const double *UY, int64_t ny,
+                   int64_t ly, int64_t width, const int64_t *slot_offsets, int32_t n_levels,
+                   int32_t order, int32_t difference, int32_t normalization, int32_t symmetric,
+                   int64_t row_begin, int64_t row_end, const double *diag_x,
+                   const double *diag_y, double *K, int64_t ldk, double *levels,
+                   void *workspace, size_t workspace_bytes, void *stream) {
+  clear_error();
+  int rc;
+  if (n_levels < 0) return fail(SK_ERR_INVALID, "n_levels must be a non-negative integer");
+  if (order < 1 || order > std::max(1, (int)n_levels))
+    return fail(SK_ERR_INVALID, "order must be the effective order in [1, max(1, n_levels)]");
+  if (normalization < SK_NORM_NONE || normalization > SK_NORM_GLOBAL)
+    return fail(SK_ERR_INVALID, "normalization must be none/levelwise/global");
+  if (!slot_offsets) return fail(SK_ERR_INVALID, "slot_offsets is NULL");
+  if ((rc = check_batch(UX, nx, lx, width, "UX"))) return rc;
+  if (symmetric) {
+    UY = UX;
+    ny = nx;
+    ly = lx;
+  } else if ((rc = check_batch(UY, ny, ly, width, "UY"))) {
+    return rc;
+  }
+  if (row_begin < 0 || row_end > nx || row_begin > row_end)
+    return fail(SK_ERR_INVALID, "row range outside [0, nx]");
+  if (!K && !levels) return fail(SK_ERR_INVALID, "K and levels are both NULL");
+  if (ldk < ny) return fail(SK_ERR_INVALID, "ldk < ny");
+  if (normalization != SK_NORM_NONE && (!diag_x || !diag_y))
+    return fail(SK_ERR_INVALID, "normalization needs diag_x and diag_y");
+  return lifted_gram(UX, nx, lx, UY, ny, ly, width, slot_offsets, n_levels, order, difference,
+                     normalization, symmetric, row_begin, row_end, diag_x, diag_y, K, ldk,
+                     levels, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int sk_lifted_self_levels(const double *UX, int64_t n, int64_t l, int64_t width,
+                          const int64_t *slot_offsets, int32_t n_levels, int32_t order,
+                          int32_t difference, double *out, void *workspace,
+                          size_t workspace_bytes, void *stream) {
+  clear_error();
+  int rc;
+  if (n_levels < 0) return fail(SK_ERR_INVALID, "n_levels must be a non-negative integer");
+  if (order < 1 || order > std::max(1, (int)n_levels))
+    return fail(SK_ERR_INVALID, "order must be the effective order in [1, max(1, n_levels)]");
+  if (!slot_offsets) return fail(SK_ERR_INVALID, "slot_offsets is NULL");
+  if ((rc = check_batch(UX, n, l, width, "UX"))) return rc;
+  if (n > 0 && !out) return fail(SK_ERR_INVALID, "out is NULL");
+  return lifted_self_levels(UX, n, l, width, slot_offsets, n_levels, order, difference, out,
+                            workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
 }  // extern "C"

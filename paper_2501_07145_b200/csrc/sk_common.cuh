@@ -198,6 +198,21 @@ int pde_self(const double *X, int64_t n, int64_t l, int64_t d, const sk_static_s
 // Upper-triangle pairwise distances (median_heuristic), float64.
 int pairwise_dist(const double *X, int64_t n, int64_t d, double *out, cudaStream_t st);
 
+// rfsf_exact_gram: static feature maps (sk_features.cu) and lifted level Grams
+// on the float64 kernel (sk_generic.cu).
+size_t static_features_workspace_bytes(const sk_feature_map &f, int64_t npts);
+int static_features(const sk_feature_map &f, const double *X, int64_t npts, int64_t d,
+                    double *out, int64_t ld_out, void *ws, size_t ws_bytes, cudaStream_t st);
+size_t lifted_workspace_bytes(int64_t npairs, int64_t ly, int M, int order, int difference);
+int lifted_gram(const double *UX, int64_t nx, int64_t lx, const double *UY, int64_t ny,
+                int64_t ly, int64_t width, const int64_t *slot_offsets, int M, int order,
+                int difference, int norm, int symmetric, int64_t row_begin, int64_t row_end,
+                const double *diag_x, const double *diag_y, double *K, int64_t ldk,
+                double *levels, void *ws, size_t ws_bytes, cudaStream_t st);
+int lifted_self_levels(const double *UX, int64_t n, int64_t l, int64_t width,
+                       const int64_t *slot_offsets, int M, int order, int difference,
+                       double *out, void *ws, size_t ws_bytes, cudaStream_t st);
+
 // Path selection: 1 fused, 2 GEMM-fed, 0 float64.
 inline int path_of(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   if (fast_supported(lx, ly, d, c)) return 1;

@@ -38,6 +38,11 @@ struct GenParams {
   StaticF64 S;
   int M, p, difference, per_level;
   int mode;  // 0 rect pairs, 1 symmetric (j >= i), 2 paired (i == j), 3 increments
+  // lifted (rfsf_exact_gram, features.py:397-424): X/Y hold per-slot static
+  // features concatenated along the channel axis; level m's point kernel is the
+  // inner product of slot m's features, channels [woff[m-1], woff[m]).
+  int lifted;
+  int woff[GEN_MAX_LEVELS + 1];
   int64_t row_begin;
   int64_t g0, count;  // pair ids [g0, g0+count) of this chunk
   double *scratch;    // [slot][count]
@@ -52,6 +57,13 @@ __device__ inline void pair_of(const GenParams &P, int64_t g, int64_t &i, int64_
     i = P.row_begin + g / P.ny;
     j = g % P.ny;
   }
+}
+
+// inner product of slot h's features of two points (level h+1's lifted point kernel)
+__device__ inline double lifted_dot(const GenParams &P, int h, const double *x, const double *y) {
+  double acc = 0.0;
+  for (int k = P.woff[h]; k < P.woff[h + 1]; ++k) acc = fma(x[k], y[k], acc);
+  return acc;
 }
 
 __global__ void __launch_bounds__(GEN_THREADS) generic_levels_kernel(GenParams P) {
@@ -75,6 +87,8 @@ __global__ void __launch_bounds__(GEN_THREADS) generic_levels_kernel(GenParams P
   double *colSY = colC + (int64_t)(M - 1) * T2 * CH;
   double *Gprev = colSY + (int64_t)(M - 1) * (p - 1) * T2 * CH;
   for (int64_t k = 0; k < (int64_t)(M - 1) * T2 * p; ++k) colC[k * CH] = 0.0;
+  const bool lifted = P.lifted != 0;
+  const int nG = lifted ? M : 1;  // Gprev rows (one per level when lifted)
 
   const double *xs = nullptr, *ys = nullptr;
   const bool from_points = P.mode != 3;
@@ -82,8 +96,12 @@ __global__ void __launch_bounds__(GEN_THREADS) generic_levels_kernel(GenParams P
     xs = P.X + i * P.lx * P.d;
     ys = (P.mode == 2 ? P.X : P.Y) + j * P.ly * P.d;
     if (P.difference)
-      for (int64_t c = 0; c < P.ly; ++c) Gprev[c * CH] = static_eval_f64(P.S, xs, ys + c * P.d, (int)P.d);
+      for (int h = 0; h < nG; ++h)
+        for (int64_t c = 0; c < P.ly; ++c)
+          Gprev[(h * P.ly + c) * CH] = lifted ? lifted_dot(P, h, xs, ys + c * P.d)
+                                              : static_eval_f64(P.S, xs, ys + c * P.d, (int)P.d);
   }
+  double gl_lev[GEN_MAX_LEVELS], a_lev[GEN_MAX_LEVELS];
 
   double s2d[GEN_MAX_LEVELS];
   double ex[GEN_MAX_LEVELS * GEN_MAX_ORDER];
@@ -98,11 +116,30 @@ __global__ void __launch_bounds__(GEN_THREADS) generic_levels_kernel(GenParams P
     double gl = 0.0;  // G(r+1, c) of the previous column
     if (from_points && P.difference) {
       xa = xs + (r + 1) * P.d;
-      gl = static_eval_f64(P.S, xa, ys, (int)P.d);
+      if (lifted)
+        for (int h = 0; h < M; ++h) gl_lev[h] = lifted_dot(P, h, xa, ys);
+      else
+        gl = static_eval_f64(P.S, xa, ys, (int)P.d);
     }
     for (int64_t c = 0; c < T2; ++c) {
       double a_shared = 0.0;
-      if (from_points) {
+      if (lifted) {
+        // per-level double difference of the slot inner products (features.py:418-419)
+        for (int h = 0; h < M; ++h) {
+          if (P.difference) {
+            double *gp = Gprev + (int64_t)h * P.ly * CH;
+            const double g11 = lifted_dot(P, h, xa, ys + (c + 1) * P.d);
+            const double g01 = gp[(c + 1) * CH];
+            const double g00 = gp[c * CH];
+            a_lev[h] = g11 - g01 - gl_lev[h] + g00;
+            gp[c * CH] = gl_lev[h];
+            if (c == T2 - 1) gp[(c + 1) * CH] = g11;
+            gl_lev[h] = g11;
+          } else {
+            a_lev[h] = lifted_dot(P, h, xs + r * P.d, ys + c * P.d);
+          }
+        }
+      } else if (from_points) {
         if (P.difference) {
           // kernels.py:281: G[1:,1:] - G[:-1,1:] - G[1:,:-1] + G[:-1,:-1]
           const double g11 = static_eval_f64(P.S, xa, ys + (c + 1) * P.d, (int)P.d);
@@ -121,8 +158,10 @@ __global__ void __launch_bounds__(GEN_THREADS) generic_levels_kernel(GenParams P
       double *Rp = Ra, *Rc = Rb;  // Rp: level m-1 at this cell, Rc: level m
       for (int m = 1; m <= M; ++m) {
         const double am =
-            (from_points || !P.per_level) ? a_shared
-                                          : P.A[(((int64_t)(m - 1) * P.count + g) * T1 + r) * T2 + c];
+            lifted ? a_lev[m - 1]
+            : (from_points || !P.per_level)
+                ? a_shared
+                : P.A[(((int64_t)(m - 1) * P.count + g) * T1 + r) * T2 + c];
         for (int k = 0; k < p * p; ++k) Rc[k] = 0.0;
         if (m == 1) {
           Rc[0] = am;
@@ -196,9 +235,9 @@ __global__ void copy_levels_kernel(const double *lv, int64_t count, int M, doubl
   if (t < count * (M + 1)) out[t] = lv[t];
 }
 
-int64_t scratch_slots(int64_t t2, int64_t ly, int M, int p) {
+int64_t scratch_slots(int64_t t2, int64_t ly, int M, int p, int lifted = 0) {
   const int64_t mm = std::max(M - 1, 0);
-  return mm * t2 * p + ly + 1;
+  return mm * t2 * p + (lifted ? std::max(M, 1) : 1) * ly + 1;
 }
 
 int64_t chunk_pairs(int64_t npairs, int64_t slots, int M) {
@@ -212,7 +251,7 @@ int64_t chunk_pairs(int64_t npairs, int64_t slots, int M) {
 int run_chunks(GenParams P, int64_t npairs, int norm, const double *diag_x,
                const double *diag_y, double *K, int64_t ldk, double *levels, double *self_out,
                void *ws, size_t ws_bytes, cudaStream_t st) {
-  const int64_t slots = scratch_slots(P.t2, P.ly, P.M, P.p);
+  const int64_t slots = scratch_slots(P.t2, P.ly, P.M, P.p, P.lifted);
   const int64_t ch = chunk_pairs(npairs, slots, P.M);
   const size_t need = (size_t)ch * (slots + P.M + 1) * sizeof(double);
   if (ws_bytes < need || ws == nullptr)
@@ -293,6 +332,79 @@ int generic_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
                         const sk_kernel_config &c, double *out, void *ws, size_t ws_bytes,
                         cudaStream_t st) {
   GenParams P = base_params(X, n, l, X, n, l, d, c);
+  P.mode = 2;
+  if (n <= 0) return SK_OK;
+  return run_chunks(P, n, SK_NORM_NONE, nullptr, nullptr, nullptr, 0, nullptr, out, ws,
+                    ws_bytes, st);
+}
+
+// --- rfsf_exact_gram's lifted level Grams (features.py:397-443), float64 ---------
+namespace {
+int lifted_params(GenParams &P, const int64_t *slot_offsets, int M, int order) {
+  if (M > GEN_MAX_LEVELS)
+    return fail(SK_ERR_UNSUPPORTED, "n_levels > " + std::to_string(GEN_MAX_LEVELS));
+  P.lifted = 1;
+  P.S = StaticF64{};
+  P.M = M;
+  P.p = std::max(1, std::min(order, std::max(M, 1)));
+  if (P.p > GEN_MAX_ORDER) return fail(SK_ERR_UNSUPPORTED, "order too large");
+  for (int m = 0; m <= M; ++m) {
+    if (slot_offsets[m] < 0 || slot_offsets[m] > P.d || (m && slot_offsets[m] < slot_offsets[m - 1]))
+      return fail(SK_ERR_INVALID, "slot_offsets must be non-decreasing within [0, width]");
+    P.woff[m] = (int)slot_offsets[m];
+  }
+  return SK_OK;
+}
+
+GenParams lifted_base(const double *UX, int64_t nx, int64_t lx, const double *UY, int64_t ny,
+                      int64_t ly, int64_t width, int difference) {
+  GenParams P{};
+  P.X = UX;
+  P.Y = UY;
+  P.nx = nx;
+  P.lx = lx;
+  P.ny = ny;
+  P.ly = ly;
+  P.d = width;
+  P.difference = difference;
+  P.t1 = difference ? std::max<int64_t>(lx - 1, 0) : lx;
+  P.t2 = difference ? std::max<int64_t>(ly - 1, 0) : ly;
+  return P;
+}
+}  // namespace
+
+size_t lifted_workspace_bytes(int64_t npairs, int64_t ly, int M, int order, int difference) {
+  const int p = std::max(1, std::min(order, std::max(M, 1)));
+  const int64_t t2 = difference ? std::max<int64_t>(ly - 1, 0) : ly;
+  const int64_t slots = scratch_slots(t2, ly, M, p, 1);
+  const int64_t ch = chunk_pairs(std::max<int64_t>(npairs, 1), slots, M);
+  return (size_t)ch * (slots + M + 1) * sizeof(double);
+}
+
+int lifted_gram(const double *UX, int64_t nx, int64_t lx, const double *UY, int64_t ny,
+                int64_t ly, int64_t width, const int64_t *slot_offsets, int M, int order,
+                int difference, int norm, int symmetric, int64_t row_begin, int64_t row_end,
+                const double *diag_x, const double *diag_y, double *K, int64_t ldk,
+                double *levels, void *ws, size_t ws_bytes, cudaStream_t st) {
+  if (symmetric) {
+    UY = UX;
+    ny = nx;
+    ly = lx;
+  }
+  GenParams P = lifted_base(UX, nx, lx, UY, ny, ly, width, difference);
+  if (int e = lifted_params(P, slot_offsets, M, order)) return e;
+  P.mode = symmetric ? 1 : 0;
+  P.row_begin = row_begin;
+  const int64_t npairs = (row_end - row_begin) * ny;
+  if (npairs <= 0) return SK_OK;
+  return run_chunks(P, npairs, norm, diag_x, diag_y, K, ldk, levels, nullptr, ws, ws_bytes, st);
+}
+
+int lifted_self_levels(const double *UX, int64_t n, int64_t l, int64_t width,
+                       const int64_t *slot_offsets, int M, int order, int difference,
+                       double *out, void *ws, size_t ws_bytes, cudaStream_t st) {
+  GenParams P = lifted_base(UX, n, l, UX, n, l, width, difference);
+  if (int e = lifted_params(P, slot_offsets, M, order)) return e;
   P.mode = 2;
   if (n <= 0) return SK_OK;
   return run_chunks(P, n, SK_NORM_NONE, nullptr, nullptr, nullptr, 0, nullptr, out, ws,

@@ -104,3 +104,38 @@ def test_oracle_pde_golden():
     for name, X, Y, sp, diff, norm, K, _, _ in _pde_cases():
         got = O.pde_gram(X, Y, sp=sp, difference=diff, normalization=norm)
         assert np.allclose(got, K, rtol=1e-12, atol=0), name
+
+
+def test_rfsf_exact_gram_oracle_matches_reference(rfsf_cases):
+    assert len(rfsf_cases) >= 10
+    for c in rfsf_cases:
+        K = O.rfsf_exact_gram(c.oracle_slots(), c.X, c.Y, M=c.M, p=c.p,
+                              difference=c.difference, normalize=c.normalize)
+        assert K.shape == c.K.shape, c.name
+        assert np.allclose(K, c.K, rtol=1e-11, atol=1e-13), c.name
+
+
+def test_rfsf_criterion06_lifted_equals_direct(rfsf_cases):
+    # test_acceptance.py:183-208: the lifted dual Gram equals the materialised
+    # rfsf_full feature inner products (max abs 1e-8)
+    n = 0
+    for c in rfsf_cases:
+        if c.direct is None:
+            continue
+        n += 1
+        assert np.abs(c.direct - c.K).max() <= 1e-8, c.name
+    assert n >= 8
+
+
+def test_rfsf_fit_rff_reproduces_reference(rfsf_cases):
+    # fit_sig_features' rff slots are host-side numpy sampling: bitwise the reference's
+    from paper_2501_07145_b200 import SeedStream
+    from paper_2501_07145_b200.features import fit_sig_features
+    for c in rfsf_cases:
+        if c.kind != "rff":
+            continue
+        st = fit_sig_features(c.state().config, c.X, SeedStream(23, (c.name,)))
+        assert len(st.slot_states) == c.M
+        for a, s in enumerate(st.slot_states):
+            assert np.array_equal(s.weights, c.slots[a]["weights"]), (c.name, a)
+            assert s.out_dim == 2 * c.D
