@@ -20,3 +20,13 @@ class NumericError(SigkernError, ArithmeticError):
 
 class NativeError(SigkernError, RuntimeError):
     """The CUDA library reported a failure (launch error, workspace, ...)."""
+
+
+class ParseError(SigkernError, ValueError):
+    """Malformed input file, with the offending line number when known (errors.py:8-15)."""
+
+    def __init__(self, message, line=None):
+        if line is not None:
+            message = f"line {line}: {message}"
+        super().__init__(message)
+        self.line = line
