@@ -28,6 +28,7 @@ os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # the CPU baseline mirrors B
 import argparse
 import json
 import subprocess
+import threading
 import sys
 import time
 
@@ -168,6 +169,11 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 
 class ClockSampler:
+    """SM clock + throttle reasons sampled DURING the timed region: NVML polled
+    every 10 ms from a thread (the data nvidia-smi reports), plus
+    `sample_now()` from the main thread while the GPU is still busy, so even a
+    sub-millisecond region (c1) gets samples. Falls back to `nvidia-smi -lms`."""
+
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -175,8 +181,43 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.nv = None
+        self.lines = []
+
+    def _nvml_line(self):
+        nv, h = self.nv, self.handle
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        flags = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                 nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        act = ["Active" if r & f else "Not Active" for f in flags]
+        return f"{sm}, {mx}, {r:#x}, " + ", ".join(act)
+
+    def sample_now(self):
+        if self.nv is not None:
+            try:
+                self.lines.append(self._nvml_line())
+            except Exception:
+                pass
+
+    def _poll(self):
+        while not self.stop.is_set():
+            self.sample_now()
+            self.stop.wait(0.01)
 
     def __enter__(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.handle = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.nv = nv
+            self.stop = threading.Event()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nv = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -187,7 +228,10 @@ class ClockSampler:
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
+        if self.nv is not None:
+            self.stop.set()
+            self.thread.join(timeout=5)
+            return
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -283,6 +327,7 @@ def run_gpu(args):
         for _ in range(args.steps):
             K = step(record=True)
         t1.record()
+        clk.sample_now()  # the queued steps are still running
         barrier()
     elapsed = t0.elapsed_time(t1)
     if world > 1:
