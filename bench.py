@@ -410,6 +410,8 @@ def run_gpu(args):
                          "path": path,
                          "flops_per_entry": F, "pairs_per_launch": pairs,
                          "order_aware_flops_per_entry": order_aware_flops_per_entry(L, d, M, p),
+                         "order_aware_frac": (pairs * order_aware_flops_per_entry(L, d, M, p)
+                                              / (g_ms / 1e3) / 1e12 / peak),
                          "kernel_ms": g_ms,
                          "peak_note": f"nominal FP32: {props.multi_processor_count} SMs x 128 "
                                       f"lanes x 2 x {sm_max:.0f} MHz (no FP32 figure in "
