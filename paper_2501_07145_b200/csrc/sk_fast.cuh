@@ -154,6 +154,17 @@ __device__ __forceinline__ void store_f4(float *dst, const float (&v)[N]) {
   for (int k = 0; k < N / 4; ++k)
     reinterpret_cast<float4 *>(dst)[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
 }
+// predicated (not branched) store: the carry writer is one lane of the warp
+template <int N>
+__device__ __forceinline__ void store_f4_if(float *dst, const float (&v)[N], bool pred) {
+#pragma unroll
+  for (int k = 0; k < N / 4; ++k)
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %5, 0;\n"
+        " @p st.global.v4.f32 [%0], {%1, %2, %3, %4};\n}\n" ::"l"(dst + 4 * k),
+        "f"(v[4 * k]), "f"(v[4 * k + 1]), "f"(v[4 * k + 2]), "f"(v[4 * k + 3]), "r"((int)pred)
+        : "memory");
+}
 template <int N>
 __device__ __forceinline__ void load_f4(float (&v)[N], const float *src) {
 #pragma unroll
@@ -515,7 +526,7 @@ struct LaneState1 : Stage {
   // level sums k_1..k_{M-1} of the pair that just completed (valid at the
   // segment's last lane at its boundary step), and k_M = kout
   __device__ __forceinline__ const float *level_sums() const { return couta; }
-  __device__ __forceinline__ void store_carry(float *dst) const {
+  __device__ __forceinline__ void store_carry(float *dst, bool pred) const {
     float buf[NHP];
 #pragma unroll
     for (int m = 0; m < NCA; ++m) {
@@ -527,7 +538,7 @@ struct LaneState1 : Stage {
     buf[2 * NCA + 2] = kout;
 #pragma unroll
     for (int k = NHM; k < NHP; ++k) buf[k] = 0.f;
-    store_f4<NHP>(dst, buf);
+    store_f4_if<NHP>(dst, buf, pred);
   }
 
   // Level recursion of one row (p = 1): R_m = A * S(R_{m-1}); cin = the
@@ -647,7 +658,7 @@ struct LaneStateG : Stage {
     for (int k = 0; k < NCH; ++k) cha[k] = chb[k] = 0.f;
   }
   __device__ __forceinline__ const float *level_sums() const { return cha; }
-  __device__ __forceinline__ void store_carry(float *dst) const {
+  __device__ __forceinline__ void store_carry(float *dst, bool pred) const {
     float buf[NHP];
 #pragma unroll
     for (int k = 0; k < NCH; ++k) {
@@ -659,7 +670,7 @@ struct LaneStateG : Stage {
     buf[2 * NCH + 2] = kout;
 #pragma unroll
     for (int k = NHM; k < NHP; ++k) buf[k] = 0.f;
-    store_f4<NHP>(dst, buf);
+    store_f4_if<NHP>(dst, buf, pred);
   }
 
   // Level recursion of one row. cin/cout: [S prefixes | E prefixes].
@@ -770,8 +781,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gram_kernel(const Params P) {
         if (head_buf) load_f4(h, cbuf + ((size_t)job * lx2 + rp) * P.nhp);
       };
       auto store_tail = [&](int64_t job, int rp) {
-        if (tail_buf && last_lane && job >= 0)
-          st.store_carry(cbuf + ((size_t)job * lx2 + rp) * P.nhp);
+        st.store_carry(cbuf + ((size_t)job * lx2 + rp) * P.nhp, tail_buf && last_lane && job >= 0);
       };
       load_head(hcur, 0, 0);
 

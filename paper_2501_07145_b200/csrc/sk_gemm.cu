@@ -86,8 +86,7 @@ __global__ void __launch_bounds__(NTHREADS) gemm_dp_kernel(const Params P) {
         if (head_buf) fast::load_f4(h, cbuf + ((size_t)job * lx2 + rp) * P.nhp);
       };
       auto store_tail = [&](int64_t job, int rp) {
-        if (tail_buf && last_lane && job >= 0)
-          st.store_carry(cbuf + ((size_t)job * lx2 + rp) * P.nhp);
+        st.store_carry(cbuf + ((size_t)job * lx2 + rp) * P.nhp, tail_buf && last_lane && job >= 0);
       };
       load_head(hcur, 0, 0);
       for (int64_t e = 0; e <= njobs; ++e) {
