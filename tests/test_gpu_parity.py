@@ -134,7 +134,7 @@ def test_ragged_lengths_and_short_sequences():
     assert np.array_equal(K, np.ones((3, 5)))
 
 
-@pytest.mark.parametrize("lx,ly", [(300, 300), (260, 600), (600, 270)])
+@pytest.mark.parametrize("lx,ly", [(300, 300), (260, 600), (600, 270), (64, 300), (65, 520)])
 def test_multi_panel_lengths(lx, ly):
     """L_y > 256: sequential 256-column panels chained through the carry buffer."""
     X = gen_brownian(6, lx, 4, SeedStream(11)).data
