@@ -237,24 +237,36 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(128 * half);
       float out[128];
 #pragma unroll
-      for (int c0 = 0; c0 < 128; c0 += 16) {
-        uint32_t v[16], w[16];
-        tmem_ld16(taddr + (uint32_t)c0, v);
-        tmem_ld16(taddr + (uint32_t)(BN + c0), w);
+      for (int c0 = 0; c0 < 128; c0 += 32) {  // two 16-column chunks of both accumulators per wait
+        uint32_t v0[16], v1[16], w0[16], w1[16];
+        tmem_ld16(taddr + (uint32_t)c0, v0);
+        tmem_ld16(taddr + (uint32_t)(c0 + 16), v1);
+        tmem_ld16(taddr + (uint32_t)(BN + c0), w0);
+        tmem_ld16(taddr + (uint32_t)(BN + c0 + 16), w1);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int j = 0; j < 16; ++j) out[c0 + j] = __uint_as_float(v[j]) + __uint_as_float(w[j]);
+        for (int j = 0; j < 16; ++j) {
+          out[c0 + j] = __uint_as_float(v0[j]) + __uint_as_float(w0[j]);
+          out[c0 + 16 + j] = __uint_as_float(v1[j]) + __uint_as_float(w1[j]);
+        }
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[0]);  // TMEM free: the next tile's MMAs may start
       aph ^= 1;
+      // C is n-major: column j of this warp is one coalesced 128-byte row
+      // segment; interior tiles store without per-element bounds checks
       const int64_t m = m0 + quad * 32 + lane;
+      const int64_t nvalid = P.Ntot - n0;
+      float *cp = Cb + n0 * P.ldc + m;
       if (m < P.Mtot) {
+        if (nvalid >= 128) {
 #pragma unroll
-        for (int j = 0; j < 128; ++j) {
-          const int64_t n = n0 + j;
-          if (n < P.Ntot) __stcs(Cb + n * P.ldc + m, out[j]);
+          for (int j = 0; j < 128; ++j) __stcs(cp + j * P.ldc, out[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 128; ++j)
+            if (j < nvalid) __stcs(cp + j * P.ldc, out[j]);
         }
       }
     }

@@ -29,3 +29,14 @@ for name, A, B, cfg in cases:
     print(f"{name:28s} path={execution_path(L, L, A.shape[2], cfg):6s} finite={bool(np.isfinite(K).all())}")
 print("levels_dp", sig_levels_dp(np.random.default_rng(0).standard_normal((3, 6, 5)), 3, order=2).shape)
 print("median", median_heuristic(X.reshape(-1, 3)))
+
+# float64 PDE kernel and rfsf_exact_gram's feature + lifted kernels
+from paper_2501_07145_b200.features import (SigFeatureConfig, StaticFeatureSpec,  # noqa: E402
+                                            fit_sig_features, rfsf_exact_gram)
+Kp = sig_kernel_gram(X[:4, :12], Y[:3, :12], cfg=KernelConfig(normalization="global"), algorithm="pde")
+print("pde", bool(np.isfinite(Kp).all()))
+for kind in ("rff", "nystroem"):
+    fc = SigFeatureConfig(variant="rfsf_full", static=StaticFeatureSpec(kind=kind), n_components=4,
+                          projection=4, n_levels=3, order=2)
+    st = fit_sig_features(fc, X[:4, :12], SeedStream(9))
+    print("rfsf", kind, bool(np.isfinite(rfsf_exact_gram(st, X[:4, :12], Y[:3, :12], normalize=True)).all()))
