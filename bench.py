@@ -277,10 +277,25 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BENCH_DIST_BACKEND=gloo: test hook that runs the multi-rank logic on ONE GPU
+    # (ranks share the device; the max-over-ranks reduce goes through host tensors)
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        tt = torch.tensor([v], device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
 
     name = args.config
     N, L, d, M, p, kind, norm, sym, _ = CONFIGS[name]
@@ -329,11 +344,7 @@ def run_gpu(args):
         t1.record()
         clk.sample_now()  # the queued steps are still running
         barrier()
-    elapsed = t0.elapsed_time(t1)
-    if world > 1:
-        tt = torch.tensor([elapsed], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        elapsed = float(tt.item())
+    elapsed = max_over_ranks(t0.elapsed_time(t1))
     ms = elapsed / args.steps
     entries = N * ny * world  # every rank's block
     value = entries / (ms / 1e3)
@@ -378,11 +389,7 @@ def run_gpu(args):
         e2e_step()
     b.record()
     barrier()
-    e_ms = a.elapsed_time(b) / args.e2e_steps
-    if world > 1:
-        tt = torch.tensor([e_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e_ms = float(tt.item())
+    e_ms = max_over_ranks(a.elapsed_time(b) / args.e2e_steps)
     h2d = Xh.nbytes + (0 if Yh is None else Yh.nbytes)
     e2e = {"value": entries / (e_ms / 1e3), "unit": "entries/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": N * ny * 8, "ms_per_step": e_ms,
