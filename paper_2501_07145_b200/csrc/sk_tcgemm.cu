@@ -19,6 +19,15 @@
 // hi*lo + lo*hi go to two TMEM accumulators (columns 0-255 and 256-511) that
 // the epilogue adds in FP32.
 //
+// 2-SM mode (SK_TC_PAIR, default): CTA pairs (clusters of 2) run
+// tcgen05.mma.cta_group::2 with M = 256: each CTA stages its own 128 A rows
+// and 128 of the tile's 256 B rows (its TMA completes on the leader's `full`
+// barrier), the leader's single thread issues the MMAs for both, commits
+// multicast to both CTAs' `empty` / `tmem_full` barriers, and each CTA drains
+// its own 128 accumulator rows from its own TMEM (the peer's epilogue arrives
+// remotely on the leader's `tmem_empty`). Per CTA this halves the B bytes
+// staged per flop (3 stages of 64 KB instead of 2 of 96 KB).
+//
 // Structure (one CTA per SM, persistent over 128 x 256 output tiles):
 //  * warp 8, one thread: TMA producer. Per stage it loads a 32-wide K slice of
 //    A_hi, A_lo (128 rows) and B_hi, B_lo (256 rows) into 128B-swizzled
@@ -36,6 +45,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <mutex>
 
 #include "sk_common.cuh"
@@ -51,9 +61,21 @@ constexpr int BN = 256;          // tile columns (B side, TMEM columns)
 constexpr int KC = SK_TC_KC;     // K floats per stage (one swizzle atom row: 128 or 64 bytes)
 constexpr int STAGES = 2 * 32 / KC;
 constexpr int SWZ_BYTES = KC * 4;  // swizzle atom width
-constexpr int A_BYTES = BM * KC * 4;  // 16 KB per part
-constexpr int B_BYTES = BN * KC * 4;  // 32 KB per part
+// PAIR: 2-SM MMA (tcgen05 cta_group::2). A cluster of two CTAs computes a
+// 256 x 256 tile: each CTA stages its own 128 rows of A and 128 of the 256 B
+// rows, the leader CTA issues M = 256 MMAs that read both CTAs' shared memory
+// and write each CTA's 128 accumulator rows into its own TMEM. Per CTA that
+// halves the B bytes staged and read from shared memory per flop.
+#ifndef SK_TC_PAIR
+#define SK_TC_PAIR 1
+#endif
+constexpr bool PAIR = SK_TC_PAIR != 0;
+constexpr int NCTA = PAIR ? 2 : 1;
+constexpr int B_ROWS = BN / NCTA;          // B rows staged per CTA
+constexpr int A_BYTES = BM * KC * 4;       // 16 KB per part
+constexpr int B_BYTES = B_ROWS * KC * 4;   // 32 KB (16 KB in PAIR mode) per part
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+constexpr int NSTAGES = PAIR ? 3 : STAGES;
 constexpr int NTHREADS = 320;  // 8 epilogue warps, producer, MMA issuer
 constexpr uint32_t TMEM_COLS = 512;
 
@@ -80,6 +102,23 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#ifdef SK_TC_DEBUG
+  for (long long it = 0;; ++it) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (it == (1ll << 24)) {
+      printf("tc hang: block %d thread %d bar %x parity %u\n", blockIdx.x, threadIdx.x,
+             smem_u32(bar), parity);
+      __trap();
+    }
+  }
+#endif
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
@@ -96,6 +135,34 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// shared::cluster address of the same object in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+// TMA into this CTA's shared memory, completing bytes on the leader CTA's barrier
+__device__ __forceinline__ void tma_load_3d_pair(void *dst, const CUtensorMap *map,
+                                                 uint32_t bar_cluster, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster)
+               : "memory");
+}
 // shared-memory matrix descriptor: K-major, 128B (or 64B) swizzle, 8-row
 // groups 8 * SWZ_BYTES apart
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
@@ -107,16 +174,24 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   d |= (uint64_t)(SWZ_BYTES == 128 ? 2 : 4) << 61;  // layout: SWIZZLE_128B / SWIZZLE_64B
   return d;
 }
-// instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = 256
+// instruction descriptor: D f32, A/B tf32, both K-major, M = 128 (256 in PAIR
+// mode: both CTAs' rows), N = 256
 constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
+                           ((uint32_t)((BM * NCTA) >> 4) << 24);
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(IDESC), "r"(acc));
+  if constexpr (PAIR)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(IDESC), "r"(acc));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(IDESC), "r"(acc));
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile(
@@ -127,10 +202,18 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
         "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
 }
+// MMA completion -> barrier (PAIR: the barrier at the same offset in both CTAs)
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
+  if constexpr (PAIR)
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+  else
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
 }
 
 __global__ void __launch_bounds__(NTHREADS, 1)
@@ -140,51 +223,76 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned stage buffers (swizzle atoms), then barriers
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t *full = (uint64_t *)(smem + STAGES * STAGE_BYTES);
-  uint64_t *empty = full + STAGES;
-  uint64_t *tfull = empty + STAGES;
+  uint64_t *full = (uint64_t *)(smem + NSTAGES * STAGE_BYTES);
+  uint64_t *empty = full + NSTAGES;
+  uint64_t *tfull = empty + NSTAGES;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < NSTAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(&tfull[0], 1);
-    mbar_init(&tempty[0], 8);  // one arrival per epilogue warp
+    mbar_init(&tempty[0], 8 * NCTA);  // one arrival per epilogue warp (of both CTAs)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (PAIR) cluster_sync();  // both CTAs' barriers exist before any remote arrive
   if (warp == 9) {  // TMEM allocation (whole warp), owner of the dealloc
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem_base = *tmem_slot;
-  const int64_t tiles_b = P.tiles_m * P.tiles_n;
+  // PAIR: tile (mc, n) of the cluster covers m-tiles 2 mc (leader) and
+  // 2 mc + 1; every CTA of the pair runs the same trip count
+  const int rank = PAIR ? (int)cluster_rank() : 0;
+  const bool leader = rank == 0;
+  const int64_t tiles_mc = (P.tiles_m + NCTA - 1) / NCTA;
+  const int64_t tiles_b = tiles_mc * P.tiles_n;
   const int64_t ntiles = tiles_b * P.batch;
+  const int64_t cid = blockIdx.x / NCTA, ncl = gridDim.x / NCTA;
 
   if (warp == 8) {
     if (lane == 0) {  // TMA producer
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int64_t t = cid; t < ntiles; t += ncl) {
         const int b = (int)(t / tiles_b), tt = (int)(t % tiles_b);
-        const int m0 = (int)((tt / P.tiles_n) * BM), n0 = (int)((tt % P.tiles_n) * BN);
+        const int m0 = (int)(((tt / P.tiles_n) * NCTA + rank) * BM);
+        const int n0 = (int)((tt % P.tiles_n) * BN + rank * B_ROWS);
         for (int kc = 0; kc < P.kchunks; ++kc) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t *st = smem + s * STAGE_BYTES;
-          mbar_expect_tx(&full[s], STAGE_BYTES);
-          tma_load_3d(st, &mAhi, &full[s], kc * KC, m0, b);
-          tma_load_3d(st + A_BYTES, &mAlo, &full[s], kc * KC, m0, b);
-          tma_load_3d(st + 2 * A_BYTES, &mBhi, &full[s], kc * KC, n0, b);
-          tma_load_3d(st + 2 * A_BYTES + B_BYTES, &mBlo, &full[s], kc * KC, n0, b);
-          if (++s == STAGES) {
+          if constexpr (PAIR) {
+            // both CTAs' bytes complete on the leader's `full` barrier
+            const uint32_t fb = mapa(smem_u32(&full[s]), 0);
+            if (leader) mbar_expect_tx(&full[s], NCTA * STAGE_BYTES);
+            tma_load_3d_pair(st, &mAhi, fb, kc * KC, m0, b);
+            tma_load_3d_pair(st + A_BYTES, &mAlo, fb, kc * KC, m0, b);
+            tma_load_3d_pair(st + 2 * A_BYTES, &mBhi, fb, kc * KC, n0, b);
+            tma_load_3d_pair(st + 2 * A_BYTES + B_BYTES, &mBlo, fb, kc * KC, n0, b);
+          } else {
+            mbar_expect_tx(&full[s], STAGE_BYTES);
+            tma_load_3d(st, &mAhi, &full[s], kc * KC, m0, b);
+            tma_load_3d(st + A_BYTES, &mAlo, &full[s], kc * KC, m0, b);
+            tma_load_3d(st + 2 * A_BYTES, &mBhi, &full[s], kc * KC, n0, b);
+            tma_load_3d(st + 2 * A_BYTES + B_BYTES, &mBlo, &full[s], kc * KC, n0, b);
+          }
+          if (++s == NSTAGES) {
             s = 0;
             ph ^= 1;
           }
@@ -192,11 +300,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp == 9) {
-    if (lane == 0) {  // MMA issuer
+    if (lane == 0 && leader) {  // MMA issuer (PAIR: the leader CTA issues for both)
       int s = 0;
       uint32_t ph = 0, aph = 0;
       const uint32_t acc_main = tmem_base, acc_corr = tmem_base + (uint32_t)BN;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int64_t t = cid; t < ntiles; t += ncl) {
         mbar_wait(&tempty[0], aph ^ 1);  // epilogue has drained the accumulators
         asm volatile("tcgen05.fence::after_thread_sync;");
         for (int kc = 0; kc < P.kchunks; ++kc) {
@@ -216,7 +324,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mma_tf32(acc_main, dah, dbh, acc);
           }
           mma_commit(&empty[s]);  // stage s is free once these MMAs retire
-          if (++s == STAGES) {
+          if (++s == NSTAGES) {
             s = 0;
             ph ^= 1;
           }
@@ -228,9 +336,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else {  // epilogue warps 0-7: TMEM lanes 32*(warp%4).., columns 128*(warp/4)..
     const int quad = warp & 3, half = warp >> 2;
     uint32_t aph = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint32_t tempty_leader = PAIR ? mapa(smem_u32(&tempty[0]), 0) : 0u;
+    for (int64_t t = cid; t < ntiles; t += ncl) {
       const int64_t b = t / tiles_b, tt = t % tiles_b;
-      const int64_t m0 = (tt / P.tiles_n) * BM, n0 = (tt % P.tiles_n) * BN + 128 * half;
+      const int64_t m0 = ((tt / P.tiles_n) * NCTA + rank) * BM, n0 = (tt % P.tiles_n) * BN + 128 * half;
       float *Cb = P.C + b * P.c_bstride;
       mbar_wait(&tfull[0], aph);
       asm volatile("tcgen05.fence::after_thread_sync;");
@@ -252,7 +361,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[0]);  // TMEM free: the next tile's MMAs may start
+      if (lane == 0) {  // TMEM free: the next tile's MMAs may start
+        if constexpr (PAIR)
+          mbar_arrive_cluster(tempty_leader);
+        else
+          mbar_arrive(&tempty[0]);
+      }
       aph ^= 1;
       // C is n-major: column j of this warp is one coalesced 128-byte row
       // segment; interior tiles store without per-element bounds checks
@@ -273,10 +387,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  __syncwarp();  // the .aligned cluster barrier needs converged warps
+  if (PAIR) cluster_sync();  // the peer is done with this CTA's smem, barriers and TMEM
   if (warp == 9) {
     asm volatile("tcgen05.fence::after_thread_sync;");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(TMEM_COLS));
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(TMEM_COLS));
   }
 }
 
@@ -351,7 +471,8 @@ int tc_gemm_3xtf32(const float *Ahi, const float *Alo, int64_t Mtot, const float
   CUtensorMap mAhi, mAlo, mBhi, mBlo;
   int rc;
   if ((rc = make_map(&mAhi, Ahi, Mtot, K, batch, BM)) || (rc = make_map(&mAlo, Alo, Mtot, K, batch, BM)) ||
-      (rc = make_map(&mBhi, Bhi, Ntot, K, batch, BN)) || (rc = make_map(&mBlo, Blo, Ntot, K, batch, BN)))
+      (rc = make_map(&mBhi, Bhi, Ntot, K, batch, B_ROWS)) ||
+      (rc = make_map(&mBlo, Blo, Ntot, K, batch, B_ROWS)))
     return rc;
   TcParams P;
   P.Mtot = Mtot;
@@ -363,12 +484,32 @@ int tc_gemm_3xtf32(const float *Ahi, const float *Alo, int64_t Mtot, const float
   P.batch = batch;
   P.c_bstride = c_bstride;
   P.C = C;
-  const size_t smem = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+  const size_t smem = 1024 + (size_t)NSTAGES * STAGE_BYTES + 256;
   SK_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-  const int grid = (int)std::min<int64_t>(P.tiles_m * P.tiles_n * batch, sm_count());
-  tc_gemm_kernel<<<grid, NTHREADS, smem, st>>>(mAhi, mAlo, mBhi, mBlo, P);
-  SK_CHECK_LAUNCH();
+  const int64_t clusters = ((P.tiles_m + NCTA - 1) / NCTA) * P.tiles_n * batch;
+  cudaLaunchConfig_t lc = {};
+  lc.blockDim = dim3(NTHREADS);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = NCTA;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  // persistent grid: as many CTA pairs as can be co-resident
+  static int resident = 0;
+  if (resident == 0) {
+    lc.gridDim = dim3((unsigned)(sm_count() / NCTA * NCTA));
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, (void *)tc_gemm_kernel, &lc) != cudaSuccess || n < 1)
+      n = sm_count() / NCTA;
+    resident = n;
+  }
+  lc.gridDim = dim3((unsigned)(std::min<int64_t>(clusters, resident) * NCTA));
+  SK_CHECK_CUDA(cudaLaunchKernelEx(&lc, tc_gemm_kernel, mAhi, mAlo, mBhi, mBlo, P));
   return SK_OK;
 }
 
