@@ -75,7 +75,7 @@ constexpr int B_ROWS = BN / NCTA;          // B rows staged per CTA
 constexpr int A_BYTES = BM * KC * 4;       // 16 KB per part
 constexpr int B_BYTES = B_ROWS * KC * 4;   // 32 KB (16 KB in PAIR mode) per part
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-constexpr int NSTAGES = PAIR ? 3 : STAGES;
+constexpr int NSTAGES = PAIR ? 3 * 32 / KC : STAGES;  // 192 KB of stages
 constexpr int NTHREADS = 320;  // 8 epilogue warps, producer, MMA issuer
 constexpr uint32_t TMEM_COLS = 512;
 
