@@ -233,6 +233,14 @@ SK_API int sk_static_features(const sk_feature_map *map, const double *X, int64_
  */
 SK_API size_t sk_lifted_workspace_bytes(int64_t npairs, int64_t ly, int32_t n_levels,
                                  int32_t order, int32_t difference);
+/* Workspace with which sk_lifted_gram precomputes the slot Grams
+ * <phi_m(x_i[r]), phi_m(y_j[c])> block by block (float64 tiled GEMM, up to
+ * 4 GiB per block) instead of forming the inner products inside the DP; with
+ * only sk_lifted_workspace_bytes(nx*ny, ...) it runs the on-the-fly kernel.
+ * sk_lifted_self_levels likewise precomputes per-sequence slot Grams with
+ * sk_lifted_gram_workspace_bytes(n, l, 1, l, ...) bytes of workspace. */
+SK_API size_t sk_lifted_gram_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly,
+                                      int32_t n_levels, int32_t order, int32_t difference);
 SK_API int sk_lifted_gram(const double *UX, int64_t nx, int64_t lx, const double *UY,
                    int64_t ny, int64_t ly, int64_t width, const int64_t *slot_offsets,
                    int32_t n_levels, int32_t order, int32_t difference,

@@ -26,7 +26,8 @@ EXPORTS = ("sk_abi_version", "sk_last_error", "sk_workspace_bytes", "sk_fast_pat
            "sk_self_levels", "sk_gram", "sk_levels_dp_workspace_bytes", "sk_levels_dp",
            "sk_increment_tensor", "sk_pairwise_dist", "sk_pde_workspace_bytes", "sk_pde_gram",
            "sk_pde_self", "sk_static_features_workspace_bytes", "sk_static_features",
-           "sk_lifted_workspace_bytes", "sk_lifted_gram", "sk_lifted_self_levels")
+           "sk_lifted_workspace_bytes", "sk_lifted_gram_workspace_bytes", "sk_lifted_gram",
+           "sk_lifted_self_levels")
 
 
 class SkStaticSpec(ctypes.Structure):
@@ -92,6 +93,8 @@ def _declare(lib):
     lib.sk_static_features.argtypes = [FMAP, P, I64, I64, P, I64, P, SZ, P]
     lib.sk_lifted_workspace_bytes.restype = SZ
     lib.sk_lifted_workspace_bytes.argtypes = [I64, I64, I32, I32, I32]
+    lib.sk_lifted_gram_workspace_bytes.restype = SZ
+    lib.sk_lifted_gram_workspace_bytes.argtypes = [I64, I64, I64, I64, I32, I32, I32]
     lib.sk_lifted_gram.restype = ctypes.c_int
     lib.sk_lifted_gram.argtypes = [P, I64, I64, P, I64, I64, I64, OFFS, I32, I32, I32, I32, I32,
                                    I64, I64, P, P, P, I64, P, P, SZ, P]

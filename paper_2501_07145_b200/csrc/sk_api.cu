@@ -286,6 +286,12 @@ size_t sk_lifted_workspace_bytes(int64_t npairs, int64_t ly, int32_t n_levels, i
   return lifted_workspace_bytes(npairs, ly, n_levels, order, difference);
 }
 
+size_t sk_lifted_gram_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly,
+                                      int32_t n_levels, int32_t order, int32_t difference) {
+  if (nx <= 0 || ny <= 0 || lx <= 0 || ly <= 0 || n_levels < 0) return 0;
+  return lifted_gram_workspace_bytes(nx, lx, ny, ly, n_levels, order, difference);
+}
+
 int sk_lifted_gram(const double *UX, int64_t nx, int64_t lx, const double *UY, int64_t ny,
                    int64_t ly, int64_t width, const int64_t *slot_offsets, int32_t n_levels,
                    int32_t order, int32_t difference, int32_t normalization, int32_t symmetric,

@@ -204,6 +204,8 @@ size_t static_features_workspace_bytes(const sk_feature_map &f, int64_t npts);
 int static_features(const sk_feature_map &f, const double *X, int64_t npts, int64_t d,
                     double *out, int64_t ld_out, void *ws, size_t ws_bytes, cudaStream_t st);
 size_t lifted_workspace_bytes(int64_t npairs, int64_t ly, int M, int order, int difference);
+size_t lifted_gram_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int M,
+                                   int order, int difference);
 int lifted_gram(const double *UX, int64_t nx, int64_t lx, const double *UY, int64_t ny,
                 int64_t ly, int64_t width, const int64_t *slot_offsets, int M, int order,
                 int difference, int norm, int symmetric, int64_t row_begin, int64_t row_end,

@@ -43,6 +43,10 @@ struct GenParams {
   // inner product of slot m's features, channels [woff[m-1], woff[m]).
   int lifted;
   int woff[GEN_MAX_LEVELS + 1];
+  // lifted with precomputed slot Grams (lifted_gram): G[h][(i - g_row0) * lx + r][j * ly + c]
+  // = <phi_h(x_i[r]), phi_h(y_j[c])>, written by dgemm_nt_kernel
+  const double *G;
+  int64_t g_ld, g_lvl, g_row0;
   int64_t row_begin;
   int64_t g0, count;  // pair ids [g0, g0+count) of this chunk
   double *scratch;    // [slot][count]
@@ -88,14 +92,18 @@ __global__ void __launch_bounds__(GEN_THREADS) generic_levels_kernel(GenParams P
   double *Gprev = colSY + (int64_t)(M - 1) * (p - 1) * T2 * CH;
   for (int64_t k = 0; k < (int64_t)(M - 1) * T2 * p; ++k) colC[k * CH] = 0.0;
   const bool lifted = P.lifted != 0;
+  const bool gmode = lifted && P.G != nullptr;  // slot Grams precomputed
   const int nG = lifted ? M : 1;  // Gprev rows (one per level when lifted)
+  const double *gx = !gmode        ? nullptr
+                     : P.mode == 2 ? P.G + i * P.lx * P.g_ld  // per-sequence self Grams
+                                   : P.G + ((i - P.g_row0) * P.lx) * P.g_ld + j * P.ly;
 
   const double *xs = nullptr, *ys = nullptr;
   const bool from_points = P.mode != 3;
   if (from_points) {
     xs = P.X + i * P.lx * P.d;
     ys = (P.mode == 2 ? P.X : P.Y) + j * P.ly * P.d;
-    if (P.difference)
+    if (P.difference && !gmode)
       for (int h = 0; h < nG; ++h)
         for (int64_t c = 0; c < P.ly; ++c)
           Gprev[(h * P.ly + c) * CH] = lifted ? lifted_dot(P, h, xs, ys + c * P.d)
@@ -114,7 +122,7 @@ __global__ void __launch_bounds__(GEN_THREADS) generic_levels_kernel(GenParams P
     for (int k = 0; k < M * p; ++k) ex[k] = 0.0;
     const double *xa = nullptr;
     double gl = 0.0;  // G(r+1, c) of the previous column
-    if (from_points && P.difference) {
+    if (from_points && P.difference && !gmode) {
       xa = xs + (r + 1) * P.d;
       if (lifted)
         for (int h = 0; h < M; ++h) gl_lev[h] = lifted_dot(P, h, xa, ys);
@@ -123,7 +131,19 @@ __global__ void __launch_bounds__(GEN_THREADS) generic_levels_kernel(GenParams P
     }
     for (int64_t c = 0; c < T2; ++c) {
       double a_shared = 0.0;
-      if (lifted) {
+      if (gmode) {
+        // per-level double difference of the slot Grams (features.py:418-419)
+        for (int h = 0; h < M; ++h) {
+          const double *gh = gx + h * P.g_lvl;
+          if (P.difference) {
+            const double g11 = gh[(r + 1) * P.g_ld + c + 1], g01 = gh[r * P.g_ld + c + 1];
+            const double g10 = gh[(r + 1) * P.g_ld + c], g00 = gh[r * P.g_ld + c];
+            a_lev[h] = g11 - g01 - g10 + g00;
+          } else {
+            a_lev[h] = gh[r * P.g_ld + c];
+          }
+        }
+      } else if (lifted) {
         // per-level double difference of the slot inner products (features.py:418-419)
         for (int h = 0; h < M; ++h) {
           if (P.difference) {
@@ -340,6 +360,63 @@ int generic_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
 
 // --- rfsf_exact_gram's lifted level Grams (features.py:397-443), float64 ---------
 namespace {
+// C[m][n] = sum_k A[m * lda + k] * B[n * ldb + k] (float64, the slot Gram
+// Ux Uy^T of _lifted_level_grams, features.py:414-415): 64 x 64 tiles, 16-wide
+// K slices staged in shared memory, 4 x 4 outputs per thread.
+constexpr int DG_T = 64, DG_K = 16;
+__global__ void __launch_bounds__(256) dgemm_nt_kernel(const double *__restrict__ A, int64_t lda,
+                                                       const double *__restrict__ B, int64_t ldb,
+                                                       int64_t Mr, int64_t Nr, int K,
+                                                       double *__restrict__ C, int64_t ldc,
+                                                       int64_t sa = 0, int64_t sb = 0,
+                                                       int64_t sc = 0) {
+  __shared__ double As[DG_K][DG_T + 1], Bs[DG_K][DG_T + 1];
+  A += blockIdx.z * sa;  // batch entry (per-sequence self Grams)
+  B += blockIdx.z * sb;
+  C += blockIdx.z * sc;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t m0 = (int64_t)blockIdx.y * DG_T, n0 = (int64_t)blockIdx.x * DG_T;
+  double acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += DG_K) {
+    for (int e = threadIdx.x; e < DG_T * DG_K; e += 256) {
+      const int row = e / DG_K, kk = e % DG_K;
+      const int64_t am = m0 + row, bn = n0 + row;
+      const bool kin = k0 + kk < K;
+      As[kk][row] = (am < Mr && kin) ? A[am * lda + k0 + kk] : 0.0;
+      Bs[kk][row] = (bn < Nr && kin) ? B[bn * ldb + k0 + kk] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < DG_K; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = As[kk][ty + 16 * u];
+        b[u] = Bs[kk][tx + 16 * u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int64_t m = m0 + ty + 16 * u, n = n0 + tx + 16 * v;
+      if (m < Mr && n < Nr) C[m * ldc + n] = acc[u][v];
+    }
+}
+
+constexpr size_t G_BLOCK_BYTES = (size_t)4 << 30;  // slot-Gram block budget
+
+int64_t g_block_rows(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int M) {
+  const size_t per_x = (size_t)std::max(M, 1) * lx * ny * ly * sizeof(double);
+  return std::max<int64_t>(1, std::min<int64_t>(nx, (int64_t)(G_BLOCK_BYTES / std::max<size_t>(per_x, 1))));
+}
+
 int lifted_params(GenParams &P, const int64_t *slot_offsets, int M, int order) {
   if (M > GEN_MAX_LEVELS)
     return fail(SK_ERR_UNSUPPORTED, "n_levels > " + std::to_string(GEN_MAX_LEVELS));
@@ -381,6 +458,13 @@ size_t lifted_workspace_bytes(int64_t npairs, int64_t ly, int M, int order, int 
   return (size_t)ch * (slots + M + 1) * sizeof(double);
 }
 
+size_t lifted_gram_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int M,
+                                   int order, int difference) {
+  const int64_t bx = g_block_rows(nx, lx, ny, ly, M);
+  const size_t g = (size_t)std::max(M, 1) * bx * lx * ny * ly * sizeof(double);
+  return lifted_workspace_bytes(bx * ny, ly, M, order, difference) + ((g + 255) & ~(size_t)255);
+}
+
 int lifted_gram(const double *UX, int64_t nx, int64_t lx, const double *UY, int64_t ny,
                 int64_t ly, int64_t width, const int64_t *slot_offsets, int M, int order,
                 int difference, int norm, int symmetric, int64_t row_begin, int64_t row_end,
@@ -394,10 +478,48 @@ int lifted_gram(const double *UX, int64_t nx, int64_t lx, const double *UY, int6
   GenParams P = lifted_base(UX, nx, lx, UY, ny, ly, width, difference);
   if (int e = lifted_params(P, slot_offsets, M, order)) return e;
   P.mode = symmetric ? 1 : 0;
-  P.row_begin = row_begin;
-  const int64_t npairs = (row_end - row_begin) * ny;
-  if (npairs <= 0) return SK_OK;
-  return run_chunks(P, npairs, norm, diag_x, diag_y, K, ldk, levels, nullptr, ws, ws_bytes, st);
+  if (row_end <= row_begin || ny <= 0) return SK_OK;
+  // Slot Grams precomputed by block of x rows when the workspace holds them
+  // (sk_lifted_gram_workspace_bytes); otherwise inner products on the fly.
+  const int64_t bx = g_block_rows(nx, lx, ny, ly, M);
+  const size_t g_bytes = (size_t)M * bx * lx * ny * ly * sizeof(double);
+  const size_t dp_bytes = lifted_workspace_bytes(bx * ny, ly, M, order, difference);
+  if (M < 1 || !ws || ws_bytes < dp_bytes + ((g_bytes + 255) & ~(size_t)255)) {
+    P.row_begin = row_begin;
+    return run_chunks(P, (row_end - row_begin) * ny, norm, diag_x, diag_y, K, ldk, levels,
+                      nullptr, ws, ws_bytes, st);
+  }
+  double *G = (double *)((char *)ws + ((dp_bytes + 255) & ~(size_t)255));
+  P.G = G;
+  P.g_ld = ny * ly;
+  P.g_lvl = bx * lx * ny * ly;
+  for (int64_t b0 = row_begin; b0 < row_end; b0 += bx) {
+    const int64_t b1 = std::min(row_end, b0 + bx), rows = (b1 - b0) * lx, cols = ny * ly;
+    for (int h = 0; h < M; ++h) {
+      const int w = P.woff[h + 1] - P.woff[h];
+      const dim3 grid((unsigned)((cols + DG_T - 1) / DG_T), (unsigned)((rows + DG_T - 1) / DG_T));
+      dgemm_nt_kernel<<<grid, 256, 0, st>>>(UX + b0 * lx * width + P.woff[h], width,
+                                            UY + P.woff[h], width, rows, cols, w,
+                                            G + h * P.g_lvl, P.g_ld);
+      SK_CHECK_LAUNCH();
+    }
+    P.g_row0 = b0;
+    P.row_begin = b0;
+    GenParams Q = P;
+    int rc;
+    if (symmetric) {
+      rc = run_chunks(Q, (b1 - b0) * ny, norm, diag_x, diag_y, K, ldk, levels, nullptr, ws,
+                      dp_bytes, st);
+    } else {
+      // cross: K / levels rows are relative to the caller's row_begin
+      rc = run_chunks(Q, (b1 - b0) * ny, norm, diag_x, diag_y,
+                      K ? K + (b0 - row_begin) * ldk : nullptr, ldk,
+                      levels ? levels + (b0 - row_begin) * ldk * (M + 1) : nullptr, nullptr, ws,
+                      dp_bytes, st);
+    }
+    if (rc) return rc;
+  }
+  return SK_OK;
 }
 
 int lifted_self_levels(const double *UX, int64_t n, int64_t l, int64_t width,
@@ -407,6 +529,27 @@ int lifted_self_levels(const double *UX, int64_t n, int64_t l, int64_t width,
   if (int e = lifted_params(P, slot_offsets, M, order)) return e;
   P.mode = 2;
   if (n <= 0) return SK_OK;
+  // per-sequence slot Grams by a batched float64 GEMM when the workspace holds
+  // them (sk_lifted_gram_workspace_bytes(n, l, 1, l, ...)), else on the fly
+  const size_t dp_bytes = lifted_workspace_bytes(n, l, M, order, difference);
+  const size_t g_bytes = (size_t)M * n * l * l * sizeof(double);
+  if (M >= 1 && ws && ws_bytes >= dp_bytes + ((g_bytes + 255) & ~(size_t)255) &&
+      n <= 65535) {
+    double *G = (double *)((char *)ws + ((dp_bytes + 255) & ~(size_t)255));
+    P.G = G;
+    P.g_ld = l;
+    P.g_lvl = n * l * l;
+    for (int h = 0; h < M; ++h) {
+      const int w = P.woff[h + 1] - P.woff[h];
+      const dim3 grid((unsigned)((l + DG_T - 1) / DG_T), (unsigned)((l + DG_T - 1) / DG_T),
+                      (unsigned)n);
+      dgemm_nt_kernel<<<grid, 256, 0, st>>>(UX + P.woff[h], width, UX + P.woff[h], width, l, l, w,
+                                            G + h * P.g_lvl, l, l * width, l * width, l * l);
+      SK_CHECK_LAUNCH();
+    }
+    return run_chunks(P, n, SK_NORM_NONE, nullptr, nullptr, nullptr, 0, nullptr, out, ws,
+                      dp_bytes, st);
+  }
   return run_chunks(P, n, SK_NORM_NONE, nullptr, nullptr, nullptr, 0, nullptr, out, ws,
                     ws_bytes, st);
 }

@@ -305,7 +305,7 @@ def rfsf_exact_gram(state, X, Y=None, normalize: bool = False, counters=None, *,
     if normalize:
         dx = _lifted_self(lib, UX, offs_c, M, p, diff)
         dy = dx if sym else _lifted_self(lib, UY, offs_c, M, p, diff)
-    buf, nb = _workspace(lib.sk_lifted_workspace_bytes(nx * ny, ly, M, p, diff), dev)
+    buf, nb = _workspace(lib.sk_lifted_gram_workspace_bytes(nx, lx, ny, ly, M, p, diff), dev)
     with torch.cuda.device(dev):
         rc = lib.sk_lifted_gram(UX.data_ptr(), nx, lx, UY.data_ptr(), ny, ly, W, offs_c, M, p,
                                 diff, norm, int(sym), 0, nx, ctypes_ptr(dx), ctypes_ptr(dy),
@@ -324,7 +324,8 @@ def _lifted_self(lib, U: torch.Tensor, offs_c, M: int, p: int, diff: int) -> tor
     out = torch.zeros((n, M + 1), dtype=torch.float64, device=U.device)
     if n == 0:
         return out
-    buf, nb = _workspace(lib.sk_lifted_workspace_bytes(n, L, M, p, diff), U.device)
+    # ny = 1, ly = L: the per-sequence slot Grams of sk_lifted_self_levels
+    buf, nb = _workspace(lib.sk_lifted_gram_workspace_bytes(n, L, 1, L, M, p, diff), U.device)
     with torch.cuda.device(U.device):
         rc = lib.sk_lifted_self_levels(U.data_ptr(), n, L, W, offs_c, M, p, diff, out.data_ptr(),
                                        ctypes_ptr(buf), nb, _stream(U.device))

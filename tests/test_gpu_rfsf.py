@@ -109,3 +109,41 @@ def test_rfsf_torch_io_and_errors():
                                             n_components=3, projection=3, n_levels=0),
                            X, SeedStream(2))
     assert np.array_equal(rfsf_exact_gram(st0, X), np.ones((3, 3)))
+
+
+@pytest.mark.parametrize("sym", [False, True])
+def test_lifted_gram_precomputed_and_on_the_fly_agree(sym):
+    """sk_lifted_gram: slot Grams precomputed by the float64 GEMM (full workspace)
+    vs inner products inside the DP (minimal workspace), and a row-block call."""
+    import ctypes
+    from paper_2501_07145_b200 import _native
+    from paper_2501_07145_b200.features import _lift
+    lib = _native.load()
+    X = gen_brownian(7, 13, 2, SeedStream(61)).data
+    Y = gen_brownian(5, 9, 2, SeedStream(62)).data
+    cfg = SigFeatureConfig(variant="rfsf_full", static=StaticFeatureSpec(kind="rff"),
+                           n_components=3, projection=3, n_levels=3, order=2)
+    st = fit_sig_features(cfg, X, SeedStream(63))
+    UX, offs = _lift(st, torch.as_tensor(X, device="cuda"))
+    UY = UX if sym else _lift(st, torch.as_tensor(Y, device="cuda"))[0]
+    nx, lx, W = UX.shape
+    ny, ly = UY.shape[:2]
+    oc = (ctypes.c_int64 * 4)(*[int(o) for o in offs])
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def run(ws_bytes, r0, r1):
+        K = torch.zeros((nx if sym else r1 - r0, ny), dtype=torch.float64, device="cuda")
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+        rc = lib.sk_lifted_gram(UX.data_ptr(), nx, lx, UY.data_ptr(), ny, ly, W, oc, 3, 2, 1, 0,
+                                int(sym), r0, r1, None, None, K.data_ptr(), ny, None,
+                                ws.data_ptr(), ws_bytes, stream)
+        assert rc == 0, lib.sk_last_error()
+        return K.cpu().numpy()
+
+    full = lib.sk_lifted_gram_workspace_bytes(nx, lx, ny, ly, 3, 2, 1)
+    small = lib.sk_lifted_workspace_bytes(nx * ny, ly, 3, 2, 1)
+    assert full > small
+    Kg, Kf = run(full, 0, nx), run(small, 0, nx)
+    assert np.allclose(Kg, Kf, rtol=1e-12, atol=1e-14)
+    if not sym:
+        assert np.allclose(run(full, 2, 6), Kg[2:6], rtol=1e-12, atol=1e-14)

@@ -4,7 +4,7 @@
 
 * PDE kernel (algorithm="pde", float64): K(X, Y), N = M' = 256, L = 64, d = 4.
 * rfsf_exact_gram (float64 lifted DP): rfsf_full rff map, D = 16, n_levels 4,
-  N = M' = 128, L = 32, d = 3.
+  N = M' = 512, L = 32, d = 3.
 * median_heuristic: 8192 points, d = 16.
 Each device number is the median of 5 CUDA-event timed calls after a warm-up,
 inputs resident on the device; the CPU number times the oracle on a bounded
@@ -60,8 +60,8 @@ res["pde"] = {"workload": "algorithm='pde' K(X,Y) N=M'=256 L=64 d=4 rbf, float64
               "device_ms": ms, "entries_per_s": 256 * 256 / (ms / 1e3),
               "cpu_oracle_entries_per_s": k * k / cs, "cpu_sample": f"{k}x{k} entries, 1 thread"}
 # rfsf_exact_gram
-Xr = gen_brownian(128, 32, 3, SeedStream(3)).data
-Yr = gen_brownian(128, 32, 3, SeedStream(4)).data
+Xr = gen_brownian(512, 32, 3, SeedStream(3)).data
+Yr = gen_brownian(512, 32, 3, SeedStream(4)).data
 fc = SigFeatureConfig(variant="rfsf_full", static=StaticFeatureSpec(kind="rff"), n_components=16,
                       projection=16, n_levels=4, order=1)
 st = fit_sig_features(fc, Xr, SeedStream(5))
@@ -71,8 +71,8 @@ k = 16
 slots = [dict(kind="rff", n_components=16, weights=s.weights) for s in st.slot_states]
 cs = cpu_s(lambda: O.rfsf_exact_gram(slots, Xr[:k], Yr[:k], M=4, p=1, normalize=True))
 res["rfsf_exact_gram"] = {
-    "workload": "rfsf_full rff D=16 (32 features/slot) n_levels=4 normalize N=M'=128 L=32 d=3, float64",
-    "device_ms": ms, "entries_per_s": 128 * 128 / (ms / 1e3),
+    "workload": "rfsf_full rff D=16 (32 features/slot) n_levels=4 normalize N=M'=512 L=32 d=3, float64",
+    "device_ms": ms, "entries_per_s": 512 * 512 / (ms / 1e3),
     "cpu_oracle_entries_per_s": k * k / cs, "cpu_sample": f"{k}x{k} entries (numpy BLAS)"}
 # median heuristic
 P = np.random.default_rng(0).standard_normal((8192, 16))
