@@ -63,6 +63,27 @@ def order_aware_flops_per_entry(L, d, M, p):
     return L * L * per_cell
 
 
+def tensor_roofline(nx, ny, L, d, kind, call_ms):
+    """3xTF32 cell-value GEMM work of one sk_gram call against the TF32 tensor peak
+    (half the MEASURED_PEAKS.json dense bf16 burst figure; B200_PROFILING's
+    2.25 PF/2 nominal if that file is absent). Timed over the whole call (GEMM + DP)."""
+    rows = 2 * ((L + 1) // 2)
+    K = ((d if kind == "linear" else d + 2) + 3) // 4 * 4  # rbf folds two n-terms (sk_gemm.cu)
+    flops = 3 * 2 * (nx * rows) * (ny * rows) * K
+    peak, src = 1125.0, "nominal 2.25 PF dense bf16 / 2 (B200_PROFILING.md fallback)"
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mp):
+        try:
+            peak = json.load(open(mp))["bf16_tflops"] / 2
+            src = "MEASURED_PEAKS.json bf16_tflops (burst) / 2"
+        except (KeyError, ValueError):
+            pass
+    achieved = flops / (call_ms / 1e3) / 1e12
+    return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s (TF32)",
+            "frac": achieved / peak, "flops_per_call": flops, "peak_source": src,
+            "note": "3 MMAs (hi*hi, hi*lo, lo*hi) per k-step; time includes the DP kernel"}
+
+
 def path_info(name):
     """(execution path, kernel label, own kernel launches per sk_gram / sk_self_levels call)."""
     from paper_2501_07145_b200.kernels import execution_path
@@ -80,8 +101,11 @@ def path_info(name):
         cols = sw * C * max(1, -(-L // (32 * C)))
         rows = 2 * ((L + 1) // 2)
         bx = max(1, min(N, (2 << 30) // (rows * N * cols * 4)))
-        return (path, "cuBLAS FP32 GEMM (cell values) + sk::gemm::gemm_dp_kernel (systolic DP)",
-                2 + -(-N // bx), 3)
+        # per x block one tcgen05 GEMM launch and one DP launch, plus the two operand packs
+        # (profiles/r1_c4_launches.txt: 32 + 32 + 2 per Gram at N = 1024)
+        return (path, "sk::tc::tc_gemm_kernel (2-SM tcgen05 3xTF32 cell values) + "
+                      "sk::gemm::gemm_dp_kernel (systolic DP); timed: the whole sk_gram call",
+                2 + 2 * -(-N // bx), 3)
     return path, "sk::generic_levels_kernel (float64)", 2, 2
 
 
@@ -427,6 +451,8 @@ def run_gpu(args):
             "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
         }
+        if path == "gemm":  # the tensor-core side, labelled (report both)
+            line["roofline"]["tensor"] = tensor_roofline(N, ny, L, d, kind, g_ms)
         if world == 1:
             line["sample_check"] = sample_check(name, K, Xh, Yh)
         print(json.dumps(line), flush=True)
