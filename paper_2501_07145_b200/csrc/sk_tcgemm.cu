@@ -45,6 +45,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <mutex>
 
@@ -499,14 +500,20 @@ int tc_gemm_3xtf32(const float *Ahi, const float *Alo, int64_t Mtot, const float
   attr[0].val.clusterDim.z = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  // persistent grid: as many CTA pairs as can be co-resident
-  static int resident = 0;
+  // persistent grid: as many CTA pairs as can be co-resident (cached per device)
+  static std::atomic<int> resident_by_dev[64];
+  int dev = 0;
+  SK_CHECK_CUDA(cudaGetDevice(&dev));
+  int resident = dev < 64 ? resident_by_dev[dev].load() : 0;
   if (resident == 0) {
     lc.gridDim = dim3((unsigned)(sm_count() / NCTA * NCTA));
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, (void *)tc_gemm_kernel, &lc) != cudaSuccess || n < 1)
+    if (cudaOccupancyMaxActiveClusters(&n, (void *)tc_gemm_kernel, &lc) != cudaSuccess || n < 1) {
+      (void)cudaGetLastError();
       n = sm_count() / NCTA;
+    }
     resident = n;
+    if (dev < 64) resident_by_dev[dev].store(n);
   }
   lc.gridDim = dim3((unsigned)(std::min<int64_t>(clusters, resident) * NCTA));
   SK_CHECK_CUDA(cudaLaunchKernelEx(&lc, tc_gemm_kernel, mAhi, mAlo, mBhi, mBlo, P));
