@@ -512,6 +512,25 @@ def test_graph_plan_matches_eager_bitwise(norm):
     print(f"c1 K(X) {norm}: graph {1e6 * tg:.0f} us/call, eager {1e6 * te:.0f} us/call")
 
 
+@pytest.mark.parametrize("kind", ["linear", "rbf"])
+def test_graph_plan_gemm_path_bitwise(kind):
+    """CUDA-graph capture of the GEMM-fed path: cluster launches of the 2-SM
+    tcgen05 GEMM (cudaLaunchKernelEx) and the DP replay bitwise."""
+    from paper_2501_07145_b200 import LinearKernel, RBFKernel, SignatureKernel
+    from paper_2501_07145_b200.kernels import execution_path
+    X = gen_brownian(9, 40, 24, SeedStream(5)).data
+    Y = gen_brownian(7, 40, 24, SeedStream(6)).data
+    static = LinearKernel() if kind == "linear" else RBFKernel()
+    norm = "none" if kind == "linear" else "levelwise"
+    eager = SignatureKernel(n_levels=3, normalization=norm, static_kernel=static)
+    graph = SignatureKernel(n_levels=3, normalization=norm, static_kernel=static, cuda_graph=True)
+    assert execution_path(40, 40, 24, eager.config if hasattr(eager, "config") else
+                          KernelConfig(static=StaticKernelSpec(kind=kind), n_levels=3,
+                                       normalization=norm)) == "gemm"
+    for A, B in ((X, Y), (X, None), (X + 0.02, Y)):
+        assert np.array_equal(graph(A, B), eager(A, B))
+
+
 def test_graph_plan_errors():
     from paper_2501_07145_b200.plan import GramPlan
     plan = GramPlan(KernelConfig(n_levels=3, normalization="global"), (4, 10, 2))
