@@ -23,10 +23,9 @@ class NativeError(SigkernError, RuntimeError):
 
 
 class ParseError(SigkernError, ValueError):
-    """Malformed input file, with the offending line number when known (errors.py:8-15)."""
+    """Malformed input file (errors.py:8-15): the text is prefixed with
+    "line N: " and `.line` holds N when the offending line is known."""
 
     def __init__(self, message, line=None):
-        if line is not None:
-            message = f"line {line}: {message}"
-        super().__init__(message)
         self.line = line
+        super().__init__(message if line is None else "line %d: %s" % (line, message))
