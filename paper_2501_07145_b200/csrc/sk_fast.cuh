@@ -325,14 +325,19 @@ struct PointStage {
       if (LINEAR) {
         ga[c] = lo;
         gb[c] = hi;
-      } else {
+      } else if constexpr (D >= 8) {
         // No clamp of the exponent at 0 (the reference clamps the float64
         // squared distance, static/kernels.py:108-114): in FP32 the norm-
         // expansion exponent near x = y carries an error of ~|x|^2 2^-23 of
         // either sign, so clamping only the positive side buys no accuracy;
-        // dropping the FMNMX measured +2.1% at c3.
+        // dropping the FMNMX measured +2.1% at c3 and +3.4% at c2. The D = 4
+        // kernels keep it: the same edit made the c5 multi-panel kernel 22%
+        // slower (its schedule is very sensitive to code changes).
         ga[c] = ex2_approx(lo);
         gb[c] = ex2_approx(hi);
+      } else {
+        ga[c] = ex2_approx(fminf(lo, 0.f));
+        gb[c] = ex2_approx(fminf(hi, 0.f));
       }
     }
   }
