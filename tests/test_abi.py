@@ -94,3 +94,40 @@ def test_invalid_arguments_rejected_before_device_work():
     assert rc == _native.SK_ERR_UNSUPPORTED
     with pytest.raises(ValueError):
         _native.check(_native.SK_ERR_INVALID, "x")
+
+
+def test_rfsf_entry_points_validate_on_the_host():
+    """sk_static_features / sk_lifted_gram / sk_lifted_self_levels reject bad
+    arguments before any device work (features.py:446-475 boundary)."""
+    lib = _native.load()
+    fm = _native.SkFeatureMap(7, 0, 4, 8, None, None, None, None, _native.SkStaticSpec(2, 3, 1.0, 1.0, 1.0, 1.0))
+    assert lib.sk_static_features(fm, None, 3, 2, None, 8, None, 0, None) == _native.SK_ERR_INVALID
+    assert b"unknown feature kind" in lib.sk_last_error()
+    fm.kind = 0  # rff: out_dim must be 2 D
+    fm.out_dim = 5
+    assert lib.sk_static_features(fm, None, 3, 2, None, 8, None, 0, None) == _native.SK_ERR_INVALID
+    assert b"out_dim" in lib.sk_last_error()
+    fm.out_dim = 8
+    assert lib.sk_static_features(fm, None, 3, 2, None, 8, None, 0, None) == _native.SK_ERR_INVALID
+    assert b"NULL" in lib.sk_last_error() or b"weights" in lib.sk_last_error()
+    assert lib.sk_static_features(fm, None, 0, 2, None, 8, None, 0, None) == _native.SK_OK  # empty
+    assert lib.sk_static_features_workspace_bytes(fm, 100) == 0
+    fm.kind, fm.out_dim = 2, 3  # nystroem: n x D landmark Gram in the workspace
+    assert lib.sk_static_features_workspace_bytes(fm, 100) == 100 * 4 * 8
+    offs = (ctypes.c_int64 * 4)(0, 2, 4, 6)
+    args = dict(nx=2, lx=5, ny=2, ly=5, width=6)
+    rc = lib.sk_lifted_gram(None, 2, 5, None, 2, 5, 6, offs, 3, 4, 1, 0, 0, 0, 2, None, None,
+                            None, 2, None, None, 0, None)
+    assert rc == _native.SK_ERR_INVALID and b"order" in lib.sk_last_error()
+    rc = lib.sk_lifted_gram(None, 2, 5, None, 2, 5, 6, None, 3, 1, 1, 0, 0, 0, 2, None, None,
+                            None, 2, None, None, 0, None)
+    assert rc == _native.SK_ERR_INVALID and b"slot_offsets" in lib.sk_last_error()
+    rc = lib.sk_lifted_gram(None, 2, 5, None, 2, 5, 6, offs, 3, 1, 1, 1, 0, 0, 2, None, None,
+                            None, 2, None, None, 0, None)
+    assert rc == _native.SK_ERR_INVALID  # UX is NULL
+    rc = lib.sk_lifted_self_levels(None, 2, 5, 6, offs, -1, 1, 1, None, None, 0, None)
+    assert rc == _native.SK_ERR_INVALID and b"n_levels" in lib.sk_last_error()
+    full = lib.sk_lifted_gram_workspace_bytes(args["nx"], args["lx"], args["ny"], args["ly"], 3, 1, 1)
+    small = lib.sk_lifted_workspace_bytes(4, 5, 3, 1, 1)
+    assert full > small > 0
+    assert lib.sk_lifted_gram_workspace_bytes(0, 5, 2, 5, 3, 1, 1) == 0
