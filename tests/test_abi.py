@@ -131,3 +131,16 @@ def test_rfsf_entry_points_validate_on_the_host():
     small = lib.sk_lifted_workspace_bytes(4, 5, 3, 1, 1)
     assert full > small > 0
     assert lib.sk_lifted_gram_workspace_bytes(0, 5, 2, 5, 3, 1, 1) == 0
+
+
+def test_pde_and_pairwise_entry_points_validate_on_the_host():
+    lib = _native.load()
+    sp = _native.SkStaticSpec(99, 3, 1.0, 1.0, 1.0, 1.0)
+    rc = lib.sk_pde_gram(None, 1, 4, None, 1, 4, 2, 0, ctypes.byref(sp), 1, 0, 1, None, 1, None, 0, None)
+    assert rc == _native.SK_ERR_INVALID and b"kind" in lib.sk_last_error()
+    sp.kind = 2
+    rc = lib.sk_pde_self(None, 1, 1, 2, ctypes.byref(sp), 1, None, None, 0, None)
+    assert rc == _native.SK_ERR_INVALID  # X NULL / one point with difference=True
+    assert lib.sk_pairwise_dist(None, 4, 0, None, None) == _native.SK_ERR_INVALID
+    assert lib.sk_pairwise_dist(None, 1, 3, None, None) == _native.SK_OK  # no pairs
+    assert lib.sk_pde_workspace_bytes(10, 5, 1) > 0
