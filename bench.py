@@ -8,15 +8,14 @@ K(X, Y) of N = M' = 8192 random-walk sequences, L = 256, d = 16, float64
 inputs generated with the reference's own generator (restated bit for bit).
 
 A "step" is one whole Gram: self levels of X and Y (normalisation) and the
-fused Gram kernel with its normalisation epilogue. With N GPUs (torchrun)
-the Gram rows partition with no exchange, so the run is weak scaling: rank r
-owns sequences [r*8192, (r+1)*8192) of X (prefix-stable generator) and
-evaluates its 8192 x 8192 block of K(X, Y); the step is timed as the max
-over ranks and `value` counts every rank's entries (no collective in the
-step; `distributed.sharded_gram` is the library call that also all-gathers
-K). `value` is entries/s with inputs resident in HBM; `e2e` is the same
-through the public API (`SignatureKernel.__call__`) from pinned host float64
-inputs to the host float64 Gram.
+fused Gram kernel with its normalisation epilogue. With N GPUs (torchrun) the
+SAME Gram is sharded (strong scaling, the north star's "8192^2 Gram sharded
+over 1/2/4/8 B200"): `distributed.sharded_gram` gives every rank a block of
+rows, and the step includes each rank's self levels, its rows and the NCCL
+all-gather that assembles K on every rank; it is timed as the max over ranks.
+`value` is entries/s with inputs resident in HBM; `e2e` is the same through
+the public API (`SignatureKernel.__call__`, or `sharded_gram` on N GPUs) from
+pinned host float64 inputs to the host float64 Gram.
 """
 
 from __future__ import annotations
@@ -47,6 +46,11 @@ CONFIGS = {
     "c4": (4096, 128, 128, 3, 1, "linear", "none", False, 16),
     "c5": (512, 2048, 4, 8, 1, "rbf", "none", False, 2),
 }
+
+
+# measured FP32 pipe rate per SM per clock (FFMA2 / FADD2 at 8 warps/SM on the
+# B200, tools/microbench/fp32_pipes.cu -> profiles/r2_fp32_pipes.txt; nominal 128)
+FP32_LANE_OPS = 127.85
 
 
 def flops_per_entry(L, d, M):
@@ -90,10 +94,13 @@ def path_info(name):
     N, L, d, M, p, kind, norm, sym, _ = CONFIGS[name]
     path = execution_path(L, L, d, kernel_config(name))
     D = 4 if d <= 4 else (8 if d <= 8 else 16)
+    # translation-invariant kinds: one midrange (centring) launch per input batch
+    mr_gram = 0 if kind == "linear" else (1 if sym else 2)
+    mr_self = 0 if kind == "linear" else 1
     if path == "fused":
         state = (f"LaneState1<PointStage<{D},8>,{M}>" if p == 1
                  else f"LaneStateG<PointStage<{D},4>,{M},{p}>")
-        return path, f"sk::fast::gram_kernel<{state}> (fused Gram)", 3, 3
+        return path, f"sk::fast::gram_kernel<{state}> (fused Gram)", 3 + mr_gram, 3 + mr_self
     if path == "gemm":
         # x blocks of the 2 GiB cell-matrix budget (sk_gemm.cu block_rows); one DP launch each
         C = 8 if p == 1 else 4
@@ -105,7 +112,7 @@ def path_info(name):
         # (profiles/r1_c4_launches.txt: 32 + 32 + 2 per Gram at N = 1024)
         return (path, "sk::tc::tc_gemm_kernel (2-SM tcgen05 3xTF32 cell values) + "
                       "sk::gemm::gemm_dp_kernel (systolic DP); timed: the whole sk_gram call",
-                2 + 2 * -(-N // bx), 3)
+                2 + 2 * -(-N // bx) + mr_gram, 3 + mr_self)
     return path, "sk::generic_levels_kernel (float64)", 2, 2
 
 
@@ -176,7 +183,7 @@ def run_reference(args):
     value = float(np.median(rates))
     line = {"metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(times)),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: gen_brownian random walks (SeedStream 1 / 2)",
             "config": workload(name), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": "entries/s", "cores": threads, "kind": "port",
@@ -296,13 +303,14 @@ def run_gpu(args):
     import torch.distributed as dist
 
     from paper_2501_07145_b200 import LinearKernel, RBFKernel, SignatureKernel
+    from paper_2501_07145_b200.distributed import _default_compute, row_blocks, sharded_gram
     from paper_2501_07145_b200.kernels import _self_levels_t, gram_block
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     # BENCH_DIST_BACKEND=gloo: test hook that runs the multi-rank logic on ONE GPU
-    # (ranks share the device; the max-over-ranks reduce goes through host tensors)
+    # (ranks share the device; collectives go through host tensors)
     backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
     if backend != "nccl":
         local %= torch.cuda.device_count()
@@ -324,32 +332,35 @@ def run_gpu(args):
     name = args.config
     N, L, d, M, p, kind, norm, sym, _ = CONFIGS[name]
     cfg = kernel_config(name)
-    # Weak scaling (the Gram partitions into independent rows): rank r owns
-    # sequences [r*N, (r+1)*N) of an (world*N)-sequence X (the prefix-stable
-    # generator makes every rank's block exact) and evaluates its N x N' row
-    # block of K(X, Y) (symmetric configs: its N x N diagonal block K(X_r)).
-    # No collective in the step; distributed.sharded_gram is the library API
-    # when every rank needs the assembled K.
-    Xh, Yh = make_inputs(name, start=rank * N)
+    # Strong scaling (the north star's "8192^2 Gram sharded over 1/2/4/8 B200"):
+    # every rank holds X and Y, evaluates its row block of the ONE fixed Gram
+    # (distributed.sharded_gram: equal row blocks for K(X, Y), paired blocks
+    # for K(X)) including the self levels of the normalisation, and one
+    # all-gather over NVLink assembles K on every rank — all inside the step.
+    Xh, Yh = make_inputs(name)
     X = torch.from_numpy(Xh).to(dev)
     Y = None if Yh is None else torch.from_numpy(Yh).to(dev)
     ny = N
 
-    # one step: self levels (normalisation) + the fused Gram of this rank's rows
-    gram_ms = []
+    gram_ms = []  # CUDA events around this rank's Gram launches
 
-    def step(record=False):
-        diag_x = diag_y = None
-        if norm != "none":
-            diag_x = _self_levels_t(X, cfg, "fp32")
-            diag_y = diag_x if Y is None else _self_levels_t(Y, cfg, "fp32")
+    def timed_compute(Xa, Ya, cfga, r0, r1, precision, K_full=None):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        diag_x = diag_y = None
+        if cfga.normalization != "none":  # self levels outside the Gram events
+            diag_x = _self_levels_t(Xa, cfga, precision)
+            diag_y = diag_x if Ya is None else _self_levels_t(Ya, cfga, precision)
         e0.record()
-        K, _ = gram_block(X, Y, cfg, diag_x=diag_x, diag_y=diag_y)
+        K, _ = gram_block(Xa, Ya, cfga, row_begin=r0, row_end=r1, precision=precision,
+                          diag_x=diag_x, diag_y=diag_y, K=K_full)
         e1.record()
-        if record:
-            gram_ms.append((e0, e1))
+        gram_ms.append((e0, e1))
         return K
+
+    def step():
+        if world == 1:
+            return timed_compute(X, Y, cfg, 0, N, "fp32", None)
+        return sharded_gram(X, Y, cfg, compute=timed_compute)
 
     def barrier():
         if world > 1:
@@ -359,23 +370,31 @@ def run_gpu(args):
     for _ in range(args.warmup):
         step()
     barrier()
+    gram_ms.clear()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         t0.record()
         for _ in range(args.steps):
-            K = step(record=True)
+            K = step()
         t1.record()
         clk.sample_now()  # the queued steps are still running
         barrier()
     elapsed = max_over_ranks(t0.elapsed_time(t1))
     ms = elapsed / args.steps
-    entries = N * ny * world  # every rank's block
+    entries = N * ny  # the one Gram, whatever the number of GPUs
     value = entries / (ms / 1e3)
 
-    # dominant kernel: the fused Gram launch (sk_gram = 2 tiny pack kernels + Gram kernel)
-    g_ms = float(np.mean([a.elapsed_time(b) for a, b in gram_ms]))
-    pairs = N * (N + 1) // 2 if sym else N * ny  # evaluated pairs of this rank's launch
+    # dominant kernel: this rank's Gram launch(es), per step
+    g_ms = float(np.sum([a.elapsed_time(b) for a, b in gram_ms])) / args.steps
+    if world == 1:
+        pairs = N * (N + 1) // 2 if sym else N * ny
+    elif sym:
+        from paper_2501_07145_b200.distributed import paired_row_blocks
+        pairs = sum(sum(N - i for i in range(a, b)) for a, b in paired_row_blocks(N, world)[rank])
+    else:
+        r0, r1 = row_blocks(N, world)[rank]
+        pairs = (r1 - r0) * ny
     F = flops_per_entry(L, d, M)
     achieved = pairs * F / (g_ms / 1e3) / 1e12
     traffic = None
@@ -387,21 +406,21 @@ def run_gpu(args):
     props = torch.cuda.get_device_properties(dev)
     clocks = clk.summary()
     sm_max = clocks["sm_max_mhz"] or 1965.0
-    peak = props.multi_processor_count * 128 * 2 * sm_max * 1e6 / 1e12
+    peak = props.multi_processor_count * FP32_LANE_OPS * 2 * sm_max * 1e6 / 1e12
 
     # end to end through the public API from pinned host buffers: the
-    # SignatureKernel facade on this rank's block (every rank, no collective)
-    import torch as _t
-    Xp = _t.from_numpy(Xh).pin_memory()
-    Yp = None if Yh is None else _t.from_numpy(Yh).pin_memory()
-    Kh = _t.empty((N, ny), dtype=_t.float64).pin_memory()
+    # SignatureKernel facade (1 GPU) or distributed.sharded_gram (N GPUs; every
+    # rank copies X and Y in and the assembled K out)
+    Xp = torch.from_numpy(Xh).pin_memory()
+    Yp = None if Yh is None else torch.from_numpy(Yh).pin_memory()
+    Kh = torch.empty((N, ny), dtype=torch.float64).pin_memory()
     static = RBFKernel(1.0) if kind == "rbf" else LinearKernel(1.0)
     sk = SignatureKernel(n_levels=M, order=p, normalization=norm, static_kernel=static)
 
     def e2e_step():
         Xd = Xp.to(dev, non_blocking=True)
         Yd = None if Yp is None else Yp.to(dev, non_blocking=True)
-        Kd = sk(Xd, Yd)
+        Kd = sk(Xd, Yd) if world == 1 else sharded_gram(Xd, Yd, cfg)
         Kh.copy_(Kd, non_blocking=True)
         return Kd
 
@@ -417,36 +436,46 @@ def run_gpu(args):
     h2d = Xh.nbytes + (0 if Yh is None else Yh.nbytes)
     e2e = {"value": entries / (e_ms / 1e3), "unit": "entries/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": N * ny * 8, "ms_per_step": e_ms,
-           "api": "SignatureKernel(...)(X, Y) on every rank's block, pinned host float64 in, "
-                  "host float64 K out (bytes per rank)"}
+           "api": ("SignatureKernel(...)(X, Y)" if world == 1 else
+                   "distributed.sharded_gram(X, Y, cfg) on every rank") +
+                  ", pinned host float64 in, host float64 K out (bytes per rank)"}
 
     path, klabel, per_gram, per_self = path_info(name)
-    launches_per_step = (per_self if norm != "none" else 0) * (1 if sym else 2) + per_gram
+    n_gram = 1 if world == 1 or not sym else 2  # symmetric: two row blocks per rank
+    launches_per_step = n_gram * ((per_self if norm != "none" else 0) * (1 if sym else 2)
+                                  + per_gram)
     if rank == 0:
+        if world == 1:
+            par = "single"
+        elif sym:
+            par = (f"paired row blocks x{world} (blocks r and {2 * world - 1}-r of {2 * world}), "
+                   f"NCCL all_gather_into_tensor of the triangle rows + bitwise mirror")
+        else:
+            par = f"row blocks x{world} of the one {N}x{ny} Gram, NCCL all_gather_into_tensor"
         line = {
             "metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "fp32 (float64 level sums and normalisation)",
             "data": "synthetic: gen_brownian random walks, SeedStream(1)/(2), reference "
                     "generator restated bit for bit",
-            "config": dict(workload(name), parallelism=(
-                f"row blocks x{world}: rank r owns sequences [r*{N}, (r+1)*{N}) of X, no collective"
-                if world > 1 else "single")),
+            "config": dict(workload(name), parallelism=par),
             "e2e": e2e,
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/traffic.json)",
-                         "kernel": klabel + ", per sk_gram call, CUDA events on its stream",
+                         "kernel": klabel + ", rank 0's sk_gram call(s) per step, CUDA events "
+                                            "on its stream",
                          "path": path,
                          "flops_per_entry": F, "pairs_per_launch": pairs,
                          "order_aware_flops_per_entry": order_aware_flops_per_entry(L, d, M, p),
                          "order_aware_frac": (pairs * order_aware_flops_per_entry(L, d, M, p)
                                               / (g_ms / 1e3) / 1e12 / peak),
                          "kernel_ms": g_ms,
-                         "peak_note": f"nominal FP32: {props.multi_processor_count} SMs x 128 "
-                                      f"lanes x 2 x {sm_max:.0f} MHz (no FP32 figure in "
-                                      f"MEASURED_PEAKS.json)"},
+                         "peak_note": f"measured FP32 pipe rate: {props.multi_processor_count} "
+                                      f"SMs x {FP32_LANE_OPS} lane-ops/clk (FFMA2/FADD2, "
+                                      f"profiles/r2_fp32_pipes.txt) x 2 x {sm_max:.0f} MHz "
+                                      f"(MEASURED_PEAKS.json has no FP32 figure)"},
             "cpu_baseline": cpu_baseline_block(name) if (world == 1 and not args.no_cpu) else None,
             "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,

@@ -1,7 +1,9 @@
-"""`gram` command of the reference CLI on the B200 path (cli.py:133-144, config.py).
+"""`gram` and `bench` commands of the reference CLI on the B200 path
+(cli.py:133-144, 197-214, config.py).
 
     python -m paper_2501_07145_b200 gram --config run.cfg [--seed S] [--output K.csv]
                                          [--threads N] [--precision fp32|fp64]
+    python -m paper_2501_07145_b200 bench --config sweep.cfg [--output bench.csv] ...
 
 Reads the reference's `key = value` config (config.py:47-76 parsing, the
 `gram` schema of config.py:157-171, 213-226 with the same defaults, casts and
@@ -11,8 +13,10 @@ CSV. Exit codes as in cli.py:252-270: 2 for config/parse errors, 1 for other
 library, value and OS errors. `--threads` is accepted for compatibility and
 ignored (the device path has no host thread pool). `--precision` is this
 build's extra flag (default fp32: the fused kernels; fp64: the float64 kernel).
-The reference's other commands (synth, features, mape, bench, classify) are
-outside this path and exit 2 with a message.
+`bench` runs the reference's sweep (config.py:217-232 schema) for its dual
+cells (benchmarks.run_bench, `bench.methods` of dual_dp / dual_pde) and
+writes the bench CSV. The reference's other commands (synth, features, mape,
+classify) are outside this path and exit 2 with a message.
 """
 
 from __future__ import annotations
@@ -22,7 +26,9 @@ import sys
 
 from .config import KERNEL_KINDS, KernelConfig, StaticKernelSpec
 from .errors import ConfigError, ParseError, SigkernError
+from .benchmarks import BENCH_METHODS, BenchSettings, run_bench, write_bench_csv
 from .kernels import ALGORITHMS, sig_kernel_gram
+from .sequences import SeedStream
 from .static_kernels import median_heuristic
 from .wire import load_sequences_csv, tabulate, write_matrix_csv
 
@@ -143,8 +149,36 @@ GRAM_SCHEMA = {
 }
 
 
+def _list_of(cast):
+    def f(k, v):
+        return [cast(k, item) for item in (v if isinstance(v, list) else [v])]
+    return f
+
+
+BENCH_SCHEMA = {  # config.py:217-232
+    "seed": (_int(0, 2 ** 64 - 1), 0),
+    "output": (_str, None),
+    "kernel.static.kind": (_choice(KERNEL_KINDS), "rbf"),
+    "kernel.static.bandwidth": (_bandwidth, "median"),
+    "bench.methods": (_list_of(_choice(BENCH_METHODS)), list(BENCH_METHODS)),
+    "bench.n_list": (_list_of(_int(1)), [10]),
+    "bench.l_list": (_list_of(_int(2)), [100]),
+    "bench.dq_list": (_list_of(_int(1)), [100]),
+    "bench.m_list": (_list_of(_int(0)), [5]),
+    "bench.dim": (_int(1), 5),
+    "bench.order": (_order, 1),
+    "bench.difference": (_bool, True),
+    "bench.mape": (_bool, False),
+    "bench.n_seeds": (_int(1), 1),
+    "bench.wall_time": (_bool, True),
+}
+
+SCHEMAS = {"gram": GRAM_SCHEMA, "bench": BENCH_SCHEMA}
+_REQUIRED = {"gram": ("input",)}
+
+
 def validate_gram_config(raw: dict, command: str = "gram") -> dict:
-    """config.py:230-267 for the `gram` command."""
+    """config.py:230-267 for the `gram` and `bench` commands."""
     file_cmd = raw.get("command")
     if file_cmd is not None and not isinstance(file_cmd, str):
         raise ConfigError(f"command: expected one of {', '.join(COMMANDS)}, got {file_cmd!r}")
@@ -156,19 +190,21 @@ def validate_gram_config(raw: dict, command: str = "gram") -> dict:
     if file_cmd is not None and file_cmd != cmd:
         raise ConfigError(
             f"command: config file says {file_cmd!r} but the CLI was invoked with {cmd!r}")
-    if cmd != "gram":
-        raise ConfigError(f"command {cmd!r} is outside the B200 Gram path (only 'gram')")
+    if cmd not in SCHEMAS:
+        raise ConfigError(f"command {cmd!r} is outside the B200 Gram path (only 'gram', 'bench')")
+    schema = SCHEMAS[cmd]
     out = {"command": cmd}
     for k, v in raw.items():
         if k == "command":
             continue
-        if k not in GRAM_SCHEMA:
+        if k not in schema:
             raise ConfigError(f"unknown config key {k!r} for command {cmd!r}")
-        out[k] = GRAM_SCHEMA[k][0](k, v)
-    for k, (_, default) in GRAM_SCHEMA.items():
+        out[k] = schema[k][0](k, v)
+    for k, (_, default) in schema.items():
         out.setdefault(k, default)
-    if out["input"] is None:
-        raise ConfigError(f"input: required for command {cmd!r}")
+    for k in _REQUIRED.get(cmd, ()):
+        if out[k] is None:
+            raise ConfigError(f"{k}: required for command {cmd!r}")
     return out
 
 
@@ -199,6 +235,20 @@ def run_gram(cfg: dict, output: str, precision: str = "fp32") -> None:
     write_matrix_csv(output, K)
 
 
+def run_bench_cmd(cfg: dict, seed: int, output: str, threads, precision: str = "fp32") -> None:
+    """cli.py:197-214: the sweep on the `bench` child stream, then the bench CSV."""
+    settings = BenchSettings(
+        methods=tuple(cfg["bench.methods"]), n_list=tuple(cfg["bench.n_list"]),
+        l_list=tuple(cfg["bench.l_list"]), dq_list=tuple(cfg["bench.dq_list"]),
+        m_list=tuple(cfg["bench.m_list"]), dim=cfg["bench.dim"], order=cfg["bench.order"],
+        difference=cfg["bench.difference"], static_kind=cfg["kernel.static.kind"],
+        bandwidth=cfg["kernel.static.bandwidth"], n_seeds=cfg["bench.n_seeds"],
+        compute_mape=cfg["bench.mape"], wall_time=cfg["bench.wall_time"])
+    records = run_bench(settings, SeedStream(seed).child("bench"), n_threads=threads or 1,
+                        precision=precision)
+    write_bench_csv(output, records)
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="paper_2501_07145_b200",
                                  description="Signature-kernel Gram matrices on B200.")
@@ -215,11 +265,14 @@ def main(argv=None) -> int:
         if not 0 <= seed < 2 ** 64:
             raise ConfigError(f"seed: expected an unsigned 64-bit integer, got {seed}")
         output = args.output or cfg["output"] or f"sigkern_{args.command}.csv"
-        run_gram(cfg, output, args.precision)
+        if args.command == "bench":
+            run_bench_cmd(cfg, seed, output, args.threads, args.precision)
+        else:
+            run_gram(cfg, output, args.precision)
     except (ConfigError, ParseError) as exc:
         print(f"error: {exc}", file=sys.stderr)
         return 2
-    except (SigkernError, ValueError, OSError) as exc:
+    except (SigkernError, ValueError, OSError, NotImplementedError) as exc:
         print(f"error: {exc}", file=sys.stderr)
         return 1
     return 0

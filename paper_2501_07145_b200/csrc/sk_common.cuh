@@ -215,6 +215,27 @@ int lifted_self_levels(const double *UX, int64_t n, int64_t l, int64_t width,
                        const int64_t *slot_offsets, int M, int order, int difference,
                        double *out, void *ws, size_t ws_bytes, cudaStream_t st);
 
+// Centring of translation-invariant static kernels on the FP32 paths: the
+// per-channel midrange c = (min + max) / 2 over every point of X (and Y) is
+// subtracted in float64 before the FP32 rounding (k(x, y) = k(x - c, y - c)).
+// The rbf point kernel's norm-expansion exponent carries an absolute FP32
+// error of ~|x'|^2 2^-24, so without it accuracy would depend on the data's
+// distance from the origin. Min and max are exact in any order, so c is
+// deterministic. `mm` holds 2d order-preserving u64 codes (min, then max).
+size_t midrange_bytes(int64_t d);
+// On success *mm_used is mm, or null when there is nothing to centre (no
+// points, or d > 1024).
+int midrange(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny, int64_t ly,
+             int64_t d, unsigned long long *mm, const unsigned long long **mm_used,
+             cudaStream_t st);
+__device__ __forceinline__ double ord_dec(unsigned long long u) {
+  return __longlong_as_double((long long)((u >> 63) ? (u & 0x7fffffffffffffffull) : ~u));
+}
+// shift of channel k (0 when mm is null)
+__device__ __forceinline__ double midrange_of(const unsigned long long *mm, int64_t d, int64_t k) {
+  return mm ? 0.5 * (ord_dec(mm[k]) + ord_dec(mm[d + k])) : 0.0;
+}
+
 // Path selection: 1 fused, 2 GEMM-fed, 0 float64.
 inline int path_of(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   if (fast_supported(lx, ly, d, c)) return 1;

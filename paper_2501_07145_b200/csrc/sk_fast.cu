@@ -13,9 +13,10 @@ namespace fast {
 // and beyond L); 2/3 difference=False (rbf / linear), x role: row 0 and rows
 // beyond L are dummies, row r holds point r-1; y role: point r, dummies
 // beyond L.
+// shift: the midrange centring of the point modes (0 and 2; sk_common.cuh).
 __device__ __forceinline__ double packed_coord(const double *__restrict__ seq, int64_t L,
                                                int64_t d, int64_t r, int k, int mode,
-                                               bool xrole, bool &dummy) {
+                                               bool xrole, double shift, bool &dummy) {
   dummy = false;
   if (mode >= 2) {
     const int64_t pt = xrole ? r - 1 : r;
@@ -23,12 +24,43 @@ __device__ __forceinline__ double packed_coord(const double *__restrict__ seq, i
       dummy = true;
       return 0.0;
     }
-    return seq[pt * d + k];
+    return mode == 2 ? seq[pt * d + k] - shift : seq[pt * d + k];
   }
   const int64_t pt = min(r, L - 1);
   double v = seq[pt * d + k];
   if (mode == 1) v = (r >= 1 && r < L) ? v - seq[(pt - 1) * d + k] : 0.0;
+  else v -= shift;
   return v;
+}
+
+__device__ __forceinline__ unsigned long long ord_enc(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// Per-channel min/max codes of `total` values laid out [..][d]. blockDim is a
+// multiple of d, and so is the grid stride: every thread sees one channel.
+__global__ void minmax_kernel(const double *__restrict__ X, int64_t total, int d,
+                              unsigned long long *__restrict__ mm) {
+  extern __shared__ unsigned long long red[];  // [2][blockDim]
+  unsigned long long lo = ~0ull, hi = 0ull;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long u = ord_enc(X[t]);
+    lo = u < lo ? u : lo;
+    hi = u > hi ? u : hi;
+  }
+  red[threadIdx.x] = lo;
+  red[blockDim.x + threadIdx.x] = hi;
+  __syncthreads();
+  if (threadIdx.x < d) {
+    for (int t = threadIdx.x + d; t < (int)blockDim.x; t += d) {
+      lo = red[t] < lo ? red[t] : lo;
+      hi = red[blockDim.x + t] > hi ? red[blockDim.x + t] : hi;
+    }
+    atomicMin(mm + threadIdx.x, lo);
+    atomicMax(mm + d + threadIdx.x, hi);
+  }
 }
 
 // n-term slot: -|x'|^2/2 for the rbf modes (-1e30 for dummies), 0 for linear
@@ -39,7 +71,7 @@ __device__ __forceinline__ float nterm(int mode, double nrm, bool dummy) {
 
 __global__ void pack_y_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
                               int64_t Lp, int D, double coord_scale, int mode,
-                              float *__restrict__ out) {
+                              const unsigned long long *__restrict__ mm, float *__restrict__ out) {
   const int YP = y_stride(D);
   const int64_t total = n * Lp;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
@@ -51,7 +83,8 @@ __global__ void pack_y_kernel(const double *__restrict__ X, int64_t n, int64_t L
     bool dummy = false;
     for (int k = 0; k < D; ++k) {
       const float v =
-          (k < d) ? (float)(packed_coord(seq, L, d, t % Lp, k, mode, false, dummy) * coord_scale)
+          (k < d) ? (float)(packed_coord(seq, L, d, t % Lp, k, mode, false, midrange_of(mm, d, k),
+                                         dummy) * coord_scale)
                   : 0.f;
       dst[k] = v;
       nrm += (double)v * (double)v;  // n-term from the rounded coordinates
@@ -63,7 +96,7 @@ __global__ void pack_y_kernel(const double *__restrict__ X, int64_t n, int64_t L
 
 __global__ void pack_x_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
                               int64_t Lp2, int D, double coord_scale, int mode,
-                              float *__restrict__ out) {
+                              const unsigned long long *__restrict__ mm, float *__restrict__ out) {
   const int XP = x_stride(D);
   const int64_t total = n * Lp2 * 2;  // one thread per (sequence, row)
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
@@ -77,7 +110,9 @@ __global__ void pack_x_kernel(const double *__restrict__ X, int64_t n, int64_t L
     bool dummy = false;
     for (int k = 0; k < D; ++k) {
       const float v =
-          (k < d) ? (float)(packed_coord(seq, L, d, r, k, mode, true, dummy) * coord_scale) : 0.f;
+          (k < d) ? (float)(packed_coord(seq, L, d, r, k, mode, true, midrange_of(mm, d, k), dummy) *
+                            coord_scale)
+                  : 0.f;
       dst[2 * k + half] = v;
       nrm += (double)v * (double)v;
     }
@@ -174,8 +209,8 @@ size_t x_bytes(int64_t n, int64_t lx, const Plan &pl) {
 size_t y_bytes(int64_t n, const Plan &pl) {
   return align256((size_t)n * lyp_of(pl) * y_stride(pl.D) * sizeof(float));
 }
-size_t roles_bytes(int64_t nx, int64_t lx, int64_t ny, const Plan &pl) {
-  return x_bytes(nx, lx, pl) + y_bytes(ny, pl) + carry_bytes(lx, pl);
+size_t roles_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t d, const Plan &pl) {
+  return x_bytes(nx, lx, pl) + y_bytes(ny, pl) + carry_bytes(lx, pl) + midrange_bytes(d);
 }
 
 double coord_scale(const sk_kernel_config &c) {
@@ -215,7 +250,7 @@ struct Packed {
 int pack_roles(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
                int64_t ly, int64_t d, const Plan &pl, const sk_kernel_config &c, void *ws,
                size_t ws_bytes, cudaStream_t st, Packed &out) {
-  const size_t need = roles_bytes(nx, lx, ny, pl);
+  const size_t need = roles_bytes(nx, lx, ny, d, pl);
   if (!ws || ws_bytes < need)
     return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
   const size_t bx = x_bytes(nx, lx, pl), by = y_bytes(ny, pl);
@@ -225,14 +260,22 @@ int pack_roles(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t
   const double cs = coord_scale(c);
   // packing mode (pack_x/pack_y): linear: A = <dx, dy> directly from increments
   const int incr = pl.nodiff ? (pl.linear ? 3 : 2) : (pl.linear ? 1 : 0);
+  // translation-invariant kinds: midrange centring (sk_common.cuh)
+  const unsigned long long *mm = nullptr;
+  if (!pl.linear) {
+    const int rc = midrange(X, nx, lx, Y == X ? nullptr : Y, ny, ly, d,
+                            (unsigned long long *)((char *)ws + bx + by + carry_bytes(lx, pl)),
+                            &mm, st);
+    if (rc) return rc;
+  }
   if (nx > 0) {
     pack_x_kernel<<<pack_blocks(nx * lx2 * 2), 256, 0, st>>>(X, nx, lx, d, lx2, pl.D, cs, incr,
-                                                             xsb);
+                                                             mm, xsb);
     SK_CHECK_LAUNCH();
   }
   if (ny > 0) {
     pack_y_kernel<<<pack_blocks(ny * lyp), 256, 0, st>>>(Y, ny, ly, d, lyp, pl.D, cs, incr,
-                                                         ysb);
+                                                         mm, ysb);
     SK_CHECK_LAUNCH();
   }
   out.xs = xsb;
@@ -273,7 +316,31 @@ size_t fast_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int6
   using namespace fast;
   const Plan pl = ny > 0 ? plan_for(lx, ly, d, c) : plan_for(lx, lx, d, c);
   if (!pl.ok) return 0;
-  return roles_bytes(nx, lx, ny > 0 ? ny : nx, pl);
+  return roles_bytes(nx, lx, ny > 0 ? ny : nx, d, pl);
+}
+
+size_t midrange_bytes(int64_t d) { return (2 * (size_t)d * 8 + 255) & ~(size_t)255; }
+
+int midrange(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny, int64_t ly,
+             int64_t d, unsigned long long *mm, const unsigned long long **mm_used,
+             cudaStream_t st) {
+  const int64_t tx = nx * lx * d, ty = Y ? ny * ly * d : 0;
+  *mm_used = nullptr;
+  if (d < 1 || d > 1024 || tx + ty == 0) return SK_OK;
+  SK_CHECK_CUDA(cudaMemsetAsync(mm, 0xff, (size_t)d * 8, st));
+  SK_CHECK_CUDA(cudaMemsetAsync(mm + d, 0, (size_t)d * 8, st));
+  const int bd = (int)(d * std::max<int64_t>(1, 256 / d));
+  const size_t sh = 2 * (size_t)bd * 8;
+  for (int r = 0; r < 2; ++r) {
+    const double *src = r ? Y : X;
+    const int64_t tot = r ? ty : tx;
+    if (tot == 0) continue;
+    const unsigned g = (unsigned)std::min<int64_t>((tot + bd - 1) / bd, (int64_t)sm_count() * 4);
+    fast::minmax_kernel<<<g, bd, sh, st>>>(src, tot, (int)d, mm);
+    SK_CHECK_LAUNCH();
+  }
+  *mm_used = mm;
+  return SK_OK;
 }
 
 int fast_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,

@@ -857,12 +857,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) gram_kernel(const Params P) {
 //  linear): the x role gets a dummy row 0 (the discarded first row of every
 //  pair), and rows/columns beyond L are dummies whose point kernel is 0 (rbf:
 //  n-term -1e30, so exp2 underflows to 0; linear: zero coordinates).
+//  mm: midrange codes (sk_common.cuh) subtracted from the points in modes 0
+//  and 2, or null.
 __global__ void pack_y_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
                               int64_t Lp, int D, double coord_scale, int mode,
-                              float *__restrict__ out);
+                              const unsigned long long *__restrict__ mm, float *__restrict__ out);
 __global__ void pack_x_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
                               int64_t Lp2, int D, double coord_scale, int mode,
-                              float *__restrict__ out);
+                              const unsigned long long *__restrict__ mm, float *__restrict__ out);
 
 int launch_d4(const Params &, int M, int order, int variant, size_t smem, cudaStream_t st);
 int launch_d8(const Params &, int M, int order, int variant, size_t smem, cudaStream_t st);

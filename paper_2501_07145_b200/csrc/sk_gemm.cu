@@ -149,6 +149,7 @@ __device__ __forceinline__ void put_split(float *hi, float *lo, int k, float v) 
 
 __global__ void pack_rows_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
                                  int64_t rows, int K, double coord_scale, int mode,
+                                 const unsigned long long *__restrict__ mm,
                                  float *__restrict__ hi, float *__restrict__ lo) {
   const int64_t total = n * rows;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
@@ -161,6 +162,7 @@ __global__ void pack_rows_kernel(const double *__restrict__ X, int64_t n, int64_
     for (int k = 0; k < d; ++k) {
       double v = seq[pt * d + k];
       if (mode == 2) v = (r >= 1 && r < L) ? v - seq[(pt - 1) * d + k] : 0.0;
+      else v -= midrange_of(mm, d, k);  // rbf: centring (sk_common.cuh)
       const float f = (float)(v * coord_scale);
       put_split(dh, dl, k, f);
       nrm += (double)f * (double)f;
@@ -199,6 +201,7 @@ Plan plan_for(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   if (c.precision != SK_PREC_FP32 || !c.difference) return pl;
   if (kind != SK_RBF && kind != SK_LINEAR) return pl;
   if (!fast::fast_orders_supported(c.n_levels, c.order)) return pl;
+  if (c.order != 1 && c.order != c.n_levels) return pl;  // DP instantiated for p = 1 and p = M
   if (kind == SK_LINEAR && c.order > 1 && c.normalization != SK_NORM_NONE) return pl;
   if (d < 1 || lx < 2 || ly < 2) return pl;
   pl.linear = kind == SK_LINEAR;
@@ -244,15 +247,17 @@ size_t operand_bytes(int64_t n, int64_t rows, const Plan &pl) {  // hi + lo
   return 2 * align256((size_t)n * rows * pl.K * 4);
 }
 
-size_t gram_bytes(int64_t nx, int64_t lx, int64_t ny, const Plan &pl) {
+// layout: x operand, y operand, cell-matrix block, carries, midrange codes
+size_t gram_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t d, const Plan &pl) {
   const int64_t bx = block_rows(nx, lx, ny, pl);
   return operand_bytes(nx, rows_x(lx), pl) + operand_bytes(ny, cols_y(pl), pl) +
-         align256((size_t)bx * rows_x(lx) * ny * cols_y(pl) * 4) + carry_bytes(lx, pl);
+         align256((size_t)bx * rows_x(lx) * ny * cols_y(pl) * 4) + carry_bytes(lx, pl) +
+         midrange_bytes(d);
 }
 
-size_t self_bytes(int64_t n, int64_t l, const Plan &pl) {
+size_t self_bytes(int64_t n, int64_t l, int64_t d, const Plan &pl) {
   return operand_bytes(n, rows_x(l), pl) + operand_bytes(n, cols_y(pl), pl) +
-         align256((size_t)n * rows_x(l) * cols_y(pl) * 4) + carry_bytes(l, pl);
+         align256((size_t)n * rows_x(l) * cols_y(pl) * 4) + carry_bytes(l, pl) + midrange_bytes(d);
 }
 
 unsigned pack_blocks(int64_t total) {
@@ -272,11 +277,12 @@ Operand carve(void *&cursor, int64_t n, int64_t rows, const Plan &pl) {
 }
 
 int pack(const double *X, int64_t n, int64_t L, int64_t d, int64_t rows, const Plan &pl,
-         const sk_kernel_config &c, bool xrole, Operand out, cudaStream_t st) {
+         const sk_kernel_config &c, bool xrole, const unsigned long long *mm, Operand out,
+         cudaStream_t st) {
   if (n <= 0) return SK_OK;
   const int mode = pl.linear ? 2 : (xrole ? 0 : 1);
   pack_rows_kernel<<<pack_blocks(n * rows), 256, 0, st>>>(X, n, L, d, rows, pl.K, coord_scale(c),
-                                                          mode, out.hi, out.lo);
+                                                          mode, mm, out.hi, out.lo);
   SK_CHECK_LAUNCH();
   return SK_OK;
 }
@@ -353,10 +359,10 @@ size_t gemm_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int6
   using namespace gemm;
   if (ny <= 0) {
     const Plan pl = plan_for(lx, lx, d, c);
-    return pl.ok ? self_bytes(nx, lx, pl) : 0;
+    return pl.ok ? self_bytes(nx, lx, d, pl) : 0;
   }
   const Plan pl = plan_for(lx, ly, d, c);
-  return pl.ok ? gram_bytes(nx, lx, ny, pl) : 0;
+  return pl.ok ? gram_bytes(nx, lx, ny, d, pl) : 0;
 }
 
 int gemm_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
@@ -372,7 +378,7 @@ int gemm_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t 
   }
   const Plan pl = plan_for(lx, ly, d, c);
   if (!pl.ok) return fail(SK_ERR_UNSUPPORTED, "gemm path does not cover this configuration");
-  const size_t need = gram_bytes(nx, lx, ny, pl);
+  const size_t need = gram_bytes(nx, lx, ny, d, pl);
   if (!ws || ws_bytes < need)
     return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
   const int64_t rx = rows_x(lx), cy = cols_y(pl), bx = block_rows(nx, lx, ny, pl);
@@ -381,8 +387,14 @@ int gemm_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t 
   const Operand yg = carve(cur, ny, cy, pl);
   float *sblk = (float *)cur;
   float *carry = (float *)((char *)sblk + align256((size_t)bx * rx * ny * cy * 4));
-  int rc = pack(X, nx, lx, d, rx, pl, c, true, xg, st);
-  if (!rc) rc = pack(Y, ny, ly, d, cy, pl, c, false, yg, st);
+  const unsigned long long *mm = nullptr;
+  if (!pl.linear) {
+    const int r = midrange(X, nx, lx, symmetric ? nullptr : Y, ny, ly, d,
+                           (unsigned long long *)((char *)carry + carry_bytes(lx, pl)), &mm, st);
+    if (r) return r;
+  }
+  int rc = pack(X, nx, lx, d, rx, pl, c, true, mm, xg, st);
+  if (!rc) rc = pack(Y, ny, ly, d, cy, pl, c, false, mm, yg, st);
   if (rc) return rc;
   if (row_end <= row_begin || ny <= 0) return SK_OK;
   Params P = base_params(pl, lx, carry);
@@ -435,7 +447,7 @@ int gemm_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
   const Plan pl = plan_for(l, l, d, c);
   if (!pl.ok) return fail(SK_ERR_UNSUPPORTED, "gemm path does not cover this configuration");
   if (n <= 0) return SK_OK;
-  const size_t need = self_bytes(n, l, pl);
+  const size_t need = self_bytes(n, l, d, pl);
   if (!ws || ws_bytes < need)
     return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
   const int64_t rx = rows_x(l), cy = cols_y(pl);
@@ -444,8 +456,14 @@ int gemm_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
   const Operand yg = carve(cur, n, cy, pl);
   float *sb = (float *)cur;
   float *carry = (float *)((char *)sb + align256((size_t)n * rx * cy * 4));
-  int rc = pack(X, n, l, d, rx, pl, c, true, xg, st);
-  if (!rc) rc = pack(X, n, l, d, cy, pl, c, false, yg, st);
+  const unsigned long long *mm = nullptr;
+  if (!pl.linear) {
+    const int r = midrange(X, n, l, nullptr, 0, 0, d,
+                           (unsigned long long *)((char *)carry + carry_bytes(l, pl)), &mm, st);
+    if (r) return r;
+  }
+  int rc = pack(X, n, l, d, rx, pl, c, true, mm, xg, st);
+  if (!rc) rc = pack(X, n, l, d, cy, pl, c, false, mm, yg, st);
   if (rc) return rc;
   // per-sequence cell matrices (pairs (i, i)): batched GEMM, [n][rx][cy]
   rc = tc_gemm_3xtf32(yg.hi, yg.lo, cy, xg.hi, xg.lo, rx, pl.K, sb, cy, n, rx * cy, st);

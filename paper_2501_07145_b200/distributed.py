@@ -8,10 +8,11 @@ NVLink/NVSwitch assembles the finished rows on every rank:
 
 * cross K(X, Y): equal row blocks, `all_gather_into_tensor` of the
   (padded) blocks;
-* symmetric K(X): rows are split so every rank gets the same number of
-  upper-triangle pairs; each rank writes its triangle rows and their mirror
-  into a zeroed full matrix and one `all_reduce(SUM)` assembles K (every
-  entry has exactly one non-zero contributor, so the sum is exact).
+* symmetric K(X): the rows are cut into 2*world equal blocks and rank r
+  evaluates the upper-triangle pairs of blocks r and 2*world-1-r (the same
+  number of pairs on every rank); one `all_gather_into_tensor` of those rows
+  (half the bytes of an all-reduce of the full matrix) and a bitwise mirror
+  of the upper triangle assemble K.
 
 `compute` is injectable so the host logic can be exercised with the gloo
 backend on CPU (tests/test_distributed.py); the default computes on the
@@ -27,7 +28,7 @@ import torch.distributed as dist
 
 from .config import KernelConfig
 
-__all__ = ["row_blocks", "triangle_row_blocks", "sharded_gram"]
+__all__ = ["row_blocks", "triangle_row_blocks", "paired_row_blocks", "sharded_gram"]
 
 
 def row_blocks(n: int, world: int) -> list[tuple[int, int]]:
@@ -52,6 +53,25 @@ def triangle_row_blocks(n: int, world: int) -> list[tuple[int, int]]:
     return [(bounds[r], bounds[r + 1]) for r in range(world)]
 
 
+def paired_row_blocks(n: int, world: int) -> list[tuple[tuple[int, int], tuple[int, int]]]:
+    """Rank r's two row blocks (r and 2*world-1-r of 2*world equal blocks): the
+    upper-triangle pair counts of the two add up to the same total on every rank."""
+    b = max(1, math.ceil(n / (2 * world))) if n else 0
+    blk = [(min(k * b, n), min((k + 1) * b, n)) for k in range(2 * world)]
+    return [(blk[r], blk[2 * world - 1 - r]) for r in range(world)]
+
+
+def _all_gather(out: torch.Tensor, inp: torch.Tensor, group) -> None:
+    """all_gather_into_tensor; a gloo group (CPU tests, or ranks sharing one GPU)
+    takes host copies of device tensors."""
+    if inp.is_cuda and dist.get_backend(group) == "gloo":
+        host = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_gather_into_tensor(host, inp.cpu(), group=group)
+        out.copy_(host)
+        return
+    dist.all_gather_into_tensor(out, inp, group=group)
+
+
 def _default_compute(X, Y, cfg, r0, r1, precision, K_full=None):
     from .kernels import gram_block
     K, _ = gram_block(X, Y, cfg, row_begin=r0, row_end=r1, precision=precision, K=K_full)
@@ -70,11 +90,28 @@ def sharded_gram(X: torch.Tensor, Y: torch.Tensor | None, cfg: KernelConfig,
     rank = dist.get_rank(group)
     nx = X.shape[0]
     if Y is None:
-        r0, r1 = triangle_row_blocks(nx, world)[rank]
-        K = torch.zeros((nx, nx), dtype=torch.float64, device=X.device)
-        compute(X, None, cfg, r0, r1, precision, K)
-        dist.all_reduce(K, op=dist.ReduceOp.SUM, group=group)
-        return K
+        blocks = paired_row_blocks(nx, world)
+        b = blocks[0][0][1] - blocks[0][0][0]  # rows per block (the last ones may be short)
+        # symmetric sk_gram calls write their rows i <= j and the mirror of
+        # them into a full local matrix; only this rank's rows are sent
+        K_loc = torch.zeros((nx, nx), dtype=torch.float64, device=X.device)
+        send = torch.zeros((2 * b, nx), dtype=torch.float64, device=X.device)
+        for k, (a0, a1) in enumerate(blocks[rank]):
+            if a1 > a0:
+                compute(X, None, cfg, a0, a1, precision, K_loc)
+                send[k * b:k * b + a1 - a0] = K_loc[a0:a1]
+        del K_loc
+        got = torch.empty((world * 2 * b, nx), dtype=torch.float64, device=X.device)
+        _all_gather(got, send, group)
+        K = torch.empty((nx, nx), dtype=torch.float64, device=X.device)
+        for r, rb in enumerate(blocks):
+            for k, (a0, a1) in enumerate(rb):
+                if a1 > a0:
+                    K[a0:a1] = got[(2 * r + k) * b:(2 * r + k) * b + a1 - a0]
+        del got
+        # rows hold the pairs i <= j; the lower triangle is their mirror (bitwise)
+        upper = torch.ones((nx, nx), dtype=torch.bool, device=X.device).triu_()
+        return torch.where(upper, K, K.T)
     ny = Y.shape[0]
     blocks = row_blocks(nx, world)
     b = blocks[0][1] - blocks[0][0]
@@ -83,5 +120,5 @@ def sharded_gram(X: torch.Tensor, Y: torch.Tensor | None, cfg: KernelConfig,
     if r1 > r0:
         local[: r1 - r0] = compute(X, Y, cfg, r0, r1, precision, None)
     out = torch.empty((b * world, ny), dtype=torch.float64, device=X.device)
-    dist.all_gather_into_tensor(out, local, group=group)
+    _all_gather(out, local, group)
     return out[:nx]

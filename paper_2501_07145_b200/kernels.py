@@ -29,7 +29,7 @@ from . import _native
 from .config import KernelConfig, LevelValues, StaticKernelSpec
 from .errors import ConfigError, NumericError
 from .sequences import SequenceBatch
-from .utils import ResourceCounters, dp_flops
+from .utils import ResourceCounters, dp_flops, gram_counts
 
 __all__ = ["sig_kernel_gram", "sig_kernel_dp", "sig_levels_dp", "increment_tensor",
            "self_levels", "uses_fast_path", "execution_path", "sig_pde_kernel"]
@@ -128,10 +128,10 @@ def _self_levels_t(Xt: torch.Tensor, cfg: KernelConfig, precision: str,
     if n == 0:
         return out
     c = c or _native.config_struct(cfg, precision)
-    if ws is None:
-        ws = _workspace(lib.sk_workspace_bytes(n, L, 0, 0, d, c), dev)
-    buf, nb = ws
-    with torch.cuda.device(dev):
+    with torch.cuda.device(dev):  # workspace sizes depend on the device's SM count
+        if ws is None:
+            ws = _workspace(lib.sk_workspace_bytes(n, L, 0, 0, d, c), dev)
+        buf, nb = ws
         rc = lib.sk_self_levels(Xt.data_ptr(), n, L, d, c, out.data_ptr(),
                                 ctypes_ptr(buf), nb, _stream(dev))
     _native.check(rc, "sk_self_levels")
@@ -156,7 +156,8 @@ def gram_block(Xt: torch.Tensor, Yt: torch.Tensor | None, cfg: KernelConfig,
     row_end = nx if row_end is None else row_end
     M = cfg.n_levels
     c = _native.config_struct(cfg, precision)
-    ws = _workspace(lib.sk_workspace_bytes(nx, lx, ny, ly, d, c), dev)
+    with torch.cuda.device(dev):  # workspace sizes depend on the device's SM count
+        ws = _workspace(lib.sk_workspace_bytes(nx, lx, ny, ly, d, c), dev)
     if cfg.normalization != "none":
         if diag_x is None:
             diag_x = _self_levels_t(Xt, cfg, precision, c, ws)
@@ -228,9 +229,10 @@ def sig_kernel_gram(X, Y=None, cfg: KernelConfig = None, algorithm: str = "dp",
         raise ValueError(f"channel mismatch: d={Xt.shape[2]} vs d={dy}")
     if algorithm == "pde":
         K = pde_gram_block(Xt, Yt, cfg)
+        _count(counters, Xt, Yt, cfg, K, "pde", tile_memory)
         return K.cpu().numpy() if was_np else K
     K, _ = gram_block(Xt, Yt, cfg, precision=precision)
-    _count(counters, Xt, Yt, cfg, K)
+    _count(counters, Xt, Yt, cfg, K, "dp", tile_memory)
     return K.cpu().numpy() if was_np else K
 
 
@@ -299,20 +301,16 @@ def sig_pde_kernel(x, y, cfg: KernelConfig, counters=None, *, device=None) -> fl
     return float(K[0, 0])
 
 
-def _count(counters, Xt, Yt, cfg, K):
+def _count(counters, Xt, Yt, cfg, K, algorithm, tile_memory):
+    """The reference's analytic counts for this call (utils.gram_counts) and the
+    device's own footprint (inputs, packed FP32 roles, K)."""
     nx, lx, d = Xt.shape
     ny, ly = (nx, lx) if Yt is None else Yt.shape[:2]
-    diff = bool(cfg.difference)
-    T1 = max(lx - 1, 0) if diff else lx
-    T2 = max(ly - 1, 0) if diff else ly
-    M, p = cfg.n_levels, cfg.effective_order
-    pairs = nx * (nx + 1) // 2 if Yt is None else nx * ny
-    counters.add_flops(dp_flops(pairs, T1, T2, d, M, p, diff))
-    if cfg.normalization != "none":
-        counters.add_flops(dp_flops(nx, T1, T1, d, M, p, diff))
-        if Yt is not None:
-            counters.add_flops(dp_flops(ny, T2, T2, d, M, p, diff))
-    counters.observe_bytes(K.numel() * 8 + (Xt.numel() + (0 if Yt is None else Yt.numel())) * 12)
+    gram_counts(counters, nx, lx, ny, ly, d, cfg.n_levels, cfg.effective_order,
+                bool(cfg.difference), cfg.normalization, Yt is None, algorithm, tile_memory)
+    if hasattr(counters, "observe_device_bytes"):
+        counters.observe_device_bytes(
+            K.numel() * 8 + (Xt.numel() + (0 if Yt is None else Yt.numel())) * 12)
 
 
 def _as_pair_points(x, dev):
@@ -326,9 +324,12 @@ def _as_pair_points(x, dev):
     return t, was_np
 
 
-def sig_kernel_dp(x, y, cfg: KernelConfig, counters=None, *, precision: str = "fp32",
+def sig_kernel_dp(x, y, cfg: KernelConfig, counters=None, *, precision: str = "fp64",
                   device=None) -> LevelValues:
-    """Level kernels k_0..k_M of one pair (kernels.py:307-312)."""
+    """Level kernels k_0..k_M of one pair (kernels.py:307-312).
+
+    Float64 by default, like the reference's per-pair values: a single pair
+    gains nothing from the FP32 Gram kernels."""
     dev = _device(device)
     xt, _ = _as_pair_points(x, dev)
     yt, _ = _as_pair_points(y, dev)

@@ -31,7 +31,8 @@ def test_library_loads_and_exports_header_symbols():
 
 def _cfg(**kw):
     st = kw.pop("static", StaticKernelSpec(kind="rbf"))
-    return _native.config_struct(KernelConfig(static=st, **kw), kw.pop("precision", "fp32"))
+    prec = kw.pop("precision", "fp32")
+    return _native.config_struct(KernelConfig(static=st, **kw), prec)
 
 
 def test_fast_path_selection():
@@ -73,7 +74,8 @@ def test_workspace_sizes():
     n, L, d = 8192, 256, 16
     ws = lib.sk_workspace_bytes(n, L, n, L, d, c3)
     # packed fp32 x role (row pairs, 2*16+4 floats) + y role (16+4 floats per point)
-    assert ws == n * (L // 2) * 36 * 4 + n * L * 20 * 4
+    # + the midrange codes of the centring (2d u64, 256-byte aligned)
+    assert ws == n * (L // 2) * 36 * 4 + n * L * 20 * 4 + 256
     f64 = _native.config_struct(KernelConfig(n_levels=3, order=2), "fp64")
     assert lib.sk_workspace_bytes(4, 6, 5, 7, 2, f64) > 0
 

@@ -91,3 +91,47 @@ def test_cli_gram_matches_reference(tmp_path, name, precision):
     tol = 1e-10 if precision == "fp64" or name.startswith("pde") else 1e-4
     assert K.shape == R.shape
     assert np.allclose(K, R, rtol=tol, atol=tol * 1e-2), np.abs(K - R).max()
+
+
+BENCH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "bench")
+BENCH_CASES = ("dual_fixed_bw", "dual_median_order", "dual_linear_nodiff")
+
+
+def test_bench_config_schema():
+    from paper_2501_07145_b200.cli import BENCH_SCHEMA
+    cfg = validate_gram_config({"bench.methods": "dual_dp", "bench.n_list": [4, 8]}, "bench")
+    assert cfg["bench.methods"] == ["dual_dp"] and cfg["bench.n_list"] == [4, 8]
+    assert cfg["kernel.static.bandwidth"] == "median" and cfg["bench.wall_time"] is True
+    assert set(cfg) == set(BENCH_SCHEMA) | {"command"}
+    with pytest.raises(ConfigError, match="bench.methods: expected one of"):
+        validate_gram_config({"bench.methods": "exact"}, "bench")
+    with pytest.raises(ConfigError, match="bench.l_list: expected an integer >= 2"):
+        validate_gram_config({"bench.l_list": 1}, "bench")
+
+
+def test_bench_primal_methods_are_outside_the_path(tmp_path, capsys):
+    cfg = tmp_path / "p.cfg"
+    cfg.write_text("command = bench\nbench.methods = dual_dp, trp\n")
+    assert main(["bench", "--config", str(cfg), "--output", str(tmp_path / "b.csv")]) == 1
+    assert "outside the B200 dual path" in capsys.readouterr().err
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", BENCH_CASES)
+def test_cli_bench_csv_bytes_match_reference(tmp_path, name):
+    """`bench` with wall_time = false: every byte of the reference's CSV (record
+    layout, F = N, flop_count and peak_bytes_est of the analytic model)."""
+    out = tmp_path / "bench.csv"
+    rc = main(["bench", "--config", os.path.join(BENCH, f"{name}.cfg"), "--output", str(out)])
+    assert rc == 0
+    assert out.read_bytes() == open(os.path.join(BENCH, f"{name}.out.csv"), "rb").read()
+
+
+@pytest.mark.gpu
+def test_run_bench_dual_dp_wall_time():
+    from paper_2501_07145_b200.benchmarks import BenchSettings, run_bench
+    from paper_2501_07145_b200.sequences import SeedStream
+    recs = run_bench(BenchSettings(methods=("dual_dp", "dual_pde"), n_list=(16,), l_list=(32,),
+                                   m_list=(3,), dim=4, bandwidth=1.0), SeedStream(5))
+    assert [r.method for r in recs] == ["dual_dp", "dual_pde"]
+    assert all(r.wall_ms > 0 and r.F == 16 and r.mape is None for r in recs)

@@ -89,6 +89,62 @@ def test_sharded_gram_gloo_world2(sym):
         assert np.array_equal(res[r], want)  # every entry has exactly one contributor
 
 
+def _gpu_worker(rank, world, port, sym, out_q):
+    """sharded_gram with its real compute: both ranks on cuda:0, gloo collectives."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2501_07145_b200 import KernelConfig, SeedStream, gen_brownian
+        torch.cuda.set_device(0)
+        X = torch.from_numpy(gen_brownian(37, 40, 5, SeedStream(3)).data).cuda()
+        Y = None if sym else torch.from_numpy(gen_brownian(29, 33, 5, SeedStream(4)).data).cuda()
+        cfg = KernelConfig(n_levels=4, normalization="levelwise")
+        K = sharded_gram(X, Y, cfg)
+        out_q.put((rank, K.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("sym", [False, True])
+def test_sharded_gram_gpu_world2_bitwise(sym):
+    """The row-sharded Gram with the rank's GPU compute equals the single-GPU
+    Gram bit for bit (cross: row blocks; symmetric: paired blocks + mirror)."""
+    from paper_2501_07145_b200 import KernelConfig, SeedStream, gen_brownian
+    from paper_2501_07145_b200.kernels import sig_kernel_gram
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, sym, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    X = gen_brownian(37, 40, 5, SeedStream(3)).data
+    Y = None if sym else gen_brownian(29, 33, 5, SeedStream(4)).data
+    want = sig_kernel_gram(X, Y, cfg=KernelConfig(n_levels=4, normalization="levelwise"))
+    for r in range(2):
+        assert np.array_equal(res[r], want)
+    if sym:
+        assert np.array_equal(res[0], res[0].T)
+
+
+def test_paired_row_blocks_balance():
+    from paper_2501_07145_b200.distributed import paired_row_blocks
+    for n in (1, 5, 64, 1000, 8192):
+        for w in (1, 2, 3, 8):
+            blocks = paired_row_blocks(n, w)
+            rows = sorted(r for rb in blocks for r in rb if r[1] > r[0])
+            assert rows[0][0] == 0 and rows[-1][1] == n
+            assert all(rows[k][1] == rows[k + 1][0] for k in range(len(rows) - 1))
+    pairs = [sum(sum(8192 - i for i in range(a, b)) for a, b in rb)
+             for rb in paired_row_blocks(8192, 8)]
+    assert max(pairs) - min(pairs) <= 8192 * 2
+
+
 def _weak_worker(rank, world, port, n, out_q):
     """bench.py's multi-GPU partition: rank r owns sequences [r*n, (r+1)*n) of X
     (prefix-stable generator) and evaluates its row block of K(X, Y); no collective
