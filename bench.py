@@ -516,12 +516,12 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
-    ap.add_argument("--n", type=int, default=None,
+    ap.add_argument("--size", type=int, default=None,
                     help="override N (profiling runs only; not a bench line)")
     args = ap.parse_args()
-    if args.n:
+    if args.size:
         c = list(CONFIGS[args.config])
-        c[0] = args.n
+        c[0] = args.size
         CONFIGS[args.config] = tuple(c)
     if args.impl == "reference":
         return run_reference(args)

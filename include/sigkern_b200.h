@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SK_ABI_VERSION 1
+#define SK_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define SK_API __attribute__((visibility("default")))
@@ -85,8 +85,13 @@ typedef struct sk_kernel_config {
   int32_t difference;     /* 1: double-differenced increments, 0: raw point kernel */
   int32_t normalization;  /* sk_normalization */
   int32_t precision;      /* sk_precision */
-  int32_t reserved;       /* must be 0 */
+  int32_t flags;          /* sk_config_flags; 0 = default */
 } sk_kernel_config;
+
+/* sk_kernel_config.flags. SK_FLAG_NO_FIXUP (diagnostics): leave the FP32
+ * paths' uncertified entries as NaN markers instead of recomputing them in
+ * float64 (see sk_gram). */
+enum sk_config_flags { SK_FLAG_NO_FIXUP = 1 };
 
 /* Library ABI version (SK_ABI_VERSION). */
 SK_API int sk_abi_version(void);
@@ -106,9 +111,13 @@ SK_API int sk_fast_path(int64_t lx, int64_t ly, int64_t d, const sk_kernel_confi
 /*
  * Self level values k_m(x_i, x_i), m = 0..n_levels, for every sequence:
  * out is (n, n_levels+1) float64.  Replaces the diagonal pass of
- * sig_kernel_gram (kernels.py:589-595).  Computed with the same kernel and
- * the same arithmetic as the diagonal of `sk_gram`, so normalised diagonals
- * are exactly 1.
+ * sig_kernel_gram (kernels.py:589-595).  The symmetric Gram's diagonal
+ * entries are formed from these values, so normalised diagonals are exactly 1.
+ * FP32 paths (difference=1): level 1 is the exact telescoped sum of the
+ * increments (kernels.py:281 summed: k(x_T,x_T) - 2k(x_0,x_T) + k(x_0,x_0),
+ * float64); a sequence whose FP32 level 1 deviates from it by more than
+ * 1e-5 relative, or with a negative or non-finite level, is recomputed in
+ * float64.
  */
 SK_API int sk_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
                    const sk_kernel_config *cfg, double *out,
@@ -117,6 +126,18 @@ SK_API int sk_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
 /*
  * Signature-kernel Gram block (kernels.py:530-600, algorithm="dp").
  *
+ *  FP32 certification: on the FP32 paths every K entry is certified in the
+ *  kernel epilogue, and entries that are not are recomputed in float64 by a
+ *  fix-up kernel in the same stream (the pair's levels and, when normalised,
+ *  both self levels), so every returned entry meets the north-star tolerance
+ *  (1e-5 relative normalised, 1e-4 unnormalised) or is float64. Level 1 is
+ *  replaced by its exact telescoped value (difference=1). An entry is
+ *  uncertified if it is non-finite, if its FP32 level 1 deviates from the
+ *  exact one by more than 1e-5 of its scale (sqrt(k_1(x,x) k_1(y,y))
+ *  normalised, sum_m |k_m(x,y)| otherwise), or if it is small against its
+ *  scale: |K| < 0.05 (normalised: the unit diagonal) or |K| < 0.01 sum_m
+ *  |k_m(x,y)| (unnormalised: cross-level cancellation). Thresholds are
+ *  calibrated on seeded sweeps.
  *  X (nx, lx, d), Y (ny, ly, d). symmetric=1 means Y is X (K(X) in the
  *  reference, `Y=None`): only pairs with i <= j are evaluated and K[i,j] is
  *  mirrored into K[j,i] bit for bit (kernels.py:449-468); Y/ny/ly are ignored.

@@ -40,7 +40,7 @@ class SkKernelConfig(ctypes.Structure):
     _fields_ = [("static_spec", SkStaticSpec), ("n_levels", ctypes.c_int32),
                 ("order", ctypes.c_int32), ("difference", ctypes.c_int32),
                 ("normalization", ctypes.c_int32), ("precision", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("flags", ctypes.c_int32)]
 
 
 class SkFeatureMap(ctypes.Structure):
@@ -118,7 +118,7 @@ def load():
                     "there is no CPU fallback")
             lib = ctypes.CDLL(LIB_PATH)
             _declare(lib)
-            if lib.sk_abi_version() != 1:
+            if lib.sk_abi_version() != 2:  # include/sigkern_b200.h SK_ABI_VERSION
                 raise RuntimeError("libsigkern_b200 ABI version mismatch")
             _lib = lib
     return _lib
@@ -139,9 +139,12 @@ def static_struct(spec) -> SkStaticSpec:
                         float(spec.gamma), float(spec.bandwidth), float(spec.alpha))
 
 
-def config_struct(cfg, precision: str = "fp32") -> SkKernelConfig:
+SK_FLAG_NO_FIXUP = 1  # include/sigkern_b200.h sk_config_flags
+
+
+def config_struct(cfg, precision: str = "fp32", flags: int = 0) -> SkKernelConfig:
     if precision not in PREC_CODES:
         raise ValueError(f"precision must be one of {tuple(PREC_CODES)}, got {precision!r}")
     return SkKernelConfig(static_struct(cfg.static), int(cfg.n_levels), int(cfg.effective_order),
                           1 if cfg.difference else 0, NORM_CODES[cfg.normalization],
-                          PREC_CODES[precision], 0)
+                          PREC_CODES[precision], int(flags))

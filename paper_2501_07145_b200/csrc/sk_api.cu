@@ -39,7 +39,7 @@ int check_config(const sk_kernel_config *c) {
     return fail(SK_ERR_INVALID, "normalization must be none/levelwise/global");
   if (c->precision != SK_PREC_FP32 && c->precision != SK_PREC_FP64)
     return fail(SK_ERR_INVALID, "precision must be SK_PREC_FP32 or SK_PREC_FP64");
-  if (c->reserved != 0) return fail(SK_ERR_INVALID, "reserved must be 0");
+  if (c->flags & ~SK_FLAG_NO_FIXUP) return fail(SK_ERR_INVALID, "unknown flags");
   return SK_OK;
 }
 
@@ -67,6 +67,19 @@ int check_generic_limits(const sk_kernel_config &c) {
     return fail(SK_ERR_UNSUPPORTED, "order > " + std::to_string(GEN_MAX_ORDER) +
                                         " is not compiled into the float64 kernel");
   return SK_OK;
+}
+
+// float64 path: the CTA-per-pair row-scan kernel at order 1 once rows have
+// >= 32 increments (below that most of a CTA would idle), else thread per pair
+bool use_rowscan(int64_t lx, int64_t ly, const sk_kernel_config &c) {
+  const int64_t T2 = c.difference ? ly - 1 : ly;
+  return rowscan_supported(lx, ly, c) && T2 >= 32;
+}
+
+int self_fixup(const double *X, int64_t n, int64_t l, int64_t d, const sk_kernel_config &c,
+               double *out, void *ws, size_t ws_bytes, cudaStream_t st) {
+  if (rowscan_supported(l, l, c)) return cert_self_fixup(X, n, l, d, c, out, ws, ws_bytes, st);
+  return fp64_self_fixup(X, n, l, d, c, out, ws, ws_bytes, st);
 }
 
 int check_batch(const double *X, int64_t n, int64_t l, int64_t d, const char *what) {
@@ -99,10 +112,18 @@ size_t sk_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int64_
   // (normalisation) and the Gram itself, each on the path it dispatches to
   auto use = [&](int64_t n1, int64_t l1, int64_t n2, int64_t l2) -> size_t {
     const int path = n2 > 0 ? path_of(l1, l2, d, *cfg) : path_of(l1, l1, d, *cfg);
-    if (path == 1) return fast_workspace_bytes(n1, l1, n2, l2, d, *cfg);
-    if (path == 2) return gemm_workspace_bytes(n1, l1, n2, l2, d, *cfg);
-    return n2 > 0 ? generic_workspace_bytes(n1 * n2, l1, l2, *cfg)
-                  : generic_workspace_bytes(n1, l1, l1, *cfg);
+    // FP32 paths: the float64 fix-up reuses the same workspace afterwards
+    // (Gram: after the FP32 level-1 buffer of the certification)
+    const int64_t l2e = n2 > 0 ? l2 : l1;
+    const size_t fix = rowscan_supported(l1, l2e, *cfg) ? cert_workspace_bytes(l1, l2e, *cfg)
+                                                         : fixup_workspace_bytes(l1, l2e, *cfg);
+    const size_t k1 = n2 > 0 ? k1buf_bytes(n1, n2) : 0;
+    if (path == 1) return k1 + std::max(fix, fast_workspace_bytes(n1, l1, n2, l2, d, *cfg));
+    if (path == 2) return k1 + std::max(fix, gemm_workspace_bytes(n1, l1, n2, l2, d, *cfg));
+    return n2 > 0 ? std::max(generic_workspace_bytes(n1 * n2, l1, l2, *cfg),
+                             rowscan_workspace_bytes(n1 * n2, l1, l2, *cfg))
+                  : std::max(generic_workspace_bytes(n1, l1, l1, *cfg),
+                             rowscan_workspace_bytes(n1, l1, l1, *cfg));
   };
   size_t need = use(nx, lx, 0, 0);
   if (ny > 0) need = std::max({need, use(ny, ly, 0, 0), use(nx, lx, ny, ly)});
@@ -118,11 +139,21 @@ int sk_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
   if ((rc = check_batch(X, n, l, d, "X"))) return rc;
   if (n > 0 && !out) return fail(SK_ERR_INVALID, "out is NULL");
   cudaStream_t st = (cudaStream_t)stream;
-  if (fast_supported(l, l, d, *cfg))
-    return fast_self_levels(X, n, l, d, *cfg, out, workspace, workspace_bytes, st);
-  if (gemm_supported(l, l, d, *cfg))
-    return gemm_self_levels(X, n, l, d, *cfg, out, workspace, workspace_bytes, st);
+  const bool fix = !(cfg->flags & SK_FLAG_NO_FIXUP);
+  if (fast_supported(l, l, d, *cfg)) {
+    rc = fast_self_levels(X, n, l, d, *cfg, out, workspace, workspace_bytes, st);
+    if (!rc && fix) rc = self_fixup(X, n, l, d, *cfg, out, workspace, workspace_bytes, st);
+    return rc;
+  }
+  if (gemm_supported(l, l, d, *cfg)) {
+    rc = gemm_self_levels(X, n, l, d, *cfg, out, workspace, workspace_bytes, st);
+    if (!rc && fix) rc = self_fixup(X, n, l, d, *cfg, out, workspace, workspace_bytes, st);
+    return rc;
+  }
   if ((rc = check_generic_limits(*cfg))) return rc;
+  if (use_rowscan(l, l, *cfg))
+    return rowscan_gram(X, n, l, X, n, l, d, 2, *cfg, 0, n, nullptr, nullptr, nullptr, 0, nullptr,
+                        out, workspace, workspace_bytes, st);
   return generic_self_levels(X, n, l, d, *cfg, out, workspace, workspace_bytes, st);
 }
 
@@ -149,15 +180,38 @@ int sk_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny
   if (cfg->normalization != SK_NORM_NONE && (!diag_x || (!symmetric && !diag_y)))
     return fail(SK_ERR_INVALID, "normalization needs diag_x and diag_y self levels");
   cudaStream_t st = (cudaStream_t)stream;
-  if (fast_supported(lx, ly, d, *cfg))
-    return fast_gram(X, nx, lx, Y, ny, ly, d, symmetric, *cfg, row_begin, row_end, diag_x,
-                     symmetric ? diag_x : diag_y, K, ldk, levels, workspace, workspace_bytes,
-                     st);
-  if (gemm_supported(lx, ly, d, *cfg))
-    return gemm_gram(X, nx, lx, Y, ny, ly, d, symmetric, *cfg, row_begin, row_end, diag_x,
-                     symmetric ? diag_x : diag_y, K, ldk, levels, workspace, workspace_bytes,
-                     st);
+  const int path = path_of(lx, ly, d, *cfg);
+  if (path != 0) {
+    // FP32 paths: [level-1 buffer of the certification | path workspace]
+    const size_t k1b = k1buf_bytes(nx, ny);
+    if (!workspace || workspace_bytes < k1b)
+      return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(k1b) + "+");
+    float *k1 = K ? (float *)workspace : nullptr;
+    void *ws = (char *)workspace + k1b;
+    const size_t wsb = workspace_bytes - k1b;
+    const double *dy = symmetric ? diag_x : diag_y;
+    if (path == 1)
+      rc = fast_gram(X, nx, lx, Y, ny, ly, d, symmetric, *cfg, row_begin, row_end, diag_x, dy, K,
+                     ldk, levels, k1, ws, wsb, st);
+    else
+      rc = gemm_gram(X, nx, lx, Y, ny, ly, d, symmetric, *cfg, row_begin, row_end, diag_x, dy, K,
+                     ldk, levels, k1, ws, wsb, st);
+    // certification pass: uncertified entries -> float64, exact level 1
+    if (!rc && K && !(cfg->flags & SK_FLAG_NO_FIXUP)) {
+      if (rowscan_supported(lx, ly, *cfg))
+        rc = cert_fixup(X, nx, lx, Y, ny, ly, d, symmetric, *cfg, row_begin, row_end, diag_x, dy,
+                        k1, K, ldk, levels, ws, wsb, st);
+      else
+        rc = fp64_fixup(X, nx, lx, Y, ny, ly, d, symmetric, *cfg, row_begin, row_end, diag_x, dy,
+                        k1, K, ldk, levels, ws, wsb, st);
+    }
+    return rc;
+  }
   if ((rc = check_generic_limits(*cfg))) return rc;
+  if (use_rowscan(lx, ly, *cfg))
+    return rowscan_gram(X, nx, lx, Y, ny, ly, d, symmetric ? 1 : 0, *cfg, row_begin, row_end,
+                        diag_x, symmetric ? diag_x : diag_y, K, ldk, levels, nullptr, workspace,
+                        workspace_bytes, st);
   return generic_gram(X, nx, lx, Y, ny, ly, d, symmetric, *cfg, row_begin, row_end, diag_x,
                       symmetric ? diag_x : diag_y, K, ldk, levels, workspace, workspace_bytes,
                       st);

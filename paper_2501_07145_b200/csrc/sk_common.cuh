@@ -60,19 +60,9 @@ __device__ inline double ipow(double b, int e) {
   return r;
 }
 
-// k(x, y) for two points (stride-1 coordinates).
-__device__ inline double static_eval_f64(const StaticF64 &S, const double *x, const double *y,
-                                         int d) {
-  double xy = 0.0;
-  for (int k = 0; k < d; ++k) xy = fma(x[k], y[k], xy);
-  if (S.kind == SK_LINEAR) return S.scale * xy;
-  if (S.kind == SK_POLYNOMIAL) return pow(S.scale * xy + S.gamma, (double)S.degree);
-  double xx = 0.0, yy = 0.0;
-  for (int k = 0; k < d; ++k) {
-    xx = fma(x[k], x[k], xx);
-    yy = fma(y[k], y[k], yy);
-  }
-  double sq = xx + yy - 2.0 * xy;
+// Static kernel from the squared distance (stationary kinds) or the inner
+// product (linear, polynomial): static/kernels.py:68-89.
+__device__ inline double static_from_sq(const StaticF64 &S, double sq) {
   if (sq < 0.0) sq = 0.0;
   const double bw2 = S.bandwidth * S.bandwidth;
   switch (S.kind) {
@@ -95,6 +85,70 @@ __device__ inline double static_eval_f64(const StaticF64 &S, const double *x, co
       return 0.0;
   }
 }
+__device__ inline double static_from_inner(const StaticF64 &S, double xy) {
+  if (S.kind == SK_LINEAR) return S.scale * xy;
+  return pow(S.scale * xy + S.gamma, (double)S.degree);
+}
+
+// k(x, y) for two points (stride-1 coordinates).
+__device__ inline double static_eval_f64(const StaticF64 &S, const double *x, const double *y,
+                                         int d) {
+  double xy = 0.0;
+  for (int k = 0; k < d; ++k) xy = fma(x[k], y[k], xy);
+  if (S.kind == SK_LINEAR || S.kind == SK_POLYNOMIAL) return static_from_inner(S, xy);
+  double xx = 0.0, yy = 0.0;
+  for (int k = 0; k < d; ++k) {
+    xx = fma(x[k], x[k], xx);
+    yy = fma(y[k], y[k], yy);
+  }
+  return static_from_sq(S, xx + yy - 2.0 * xy);
+}
+
+// Exact level 1 of a pair (difference=True): the increments telescope,
+// sum_ij A_ij = k(x_T, y_T') - k(x_0, y_T') - k(x_T, y_0) + k(x_0, y_0)
+// (kernels.py:281 summed over the grid; the level-1 identity of
+// test_kernels.py:130-140). x, y are the sequences' float64 points.
+__device__ inline double exact_level1(const StaticF64 &S, const double *x, int64_t lx,
+                                      const double *y, int64_t ly, int d) {
+  if (lx < 2 || ly < 2) return 0.0;
+  const double *xT = x + (lx - 1) * d, *yT = y + (ly - 1) * d;
+  double s00 = 0.0, s01 = 0.0, s10 = 0.0, s11 = 0.0;  // one pass over the four corners
+  if (S.kind == SK_LINEAR || S.kind == SK_POLYNOMIAL) {
+    for (int k = 0; k < d; ++k) {
+      const double a0 = x[k], a1 = xT[k], b0 = y[k], b1 = yT[k];
+      s00 = fma(a0, b0, s00);
+      s01 = fma(a0, b1, s01);
+      s10 = fma(a1, b0, s10);
+      s11 = fma(a1, b1, s11);
+    }
+    return static_from_inner(S, s11) - static_from_inner(S, s01) - static_from_inner(S, s10) +
+           static_from_inner(S, s00);
+  }
+  for (int k = 0; k < d; ++k) {  // stationary kinds: direct squared distances
+    const double a0 = x[k], a1 = xT[k], b0 = y[k], b1 = yT[k];
+    s00 = fma(a0 - b0, a0 - b0, s00);
+    s01 = fma(a0 - b1, a0 - b1, s01);
+    s10 = fma(a1 - b0, a1 - b0, s10);
+    s11 = fma(a1 - b1, a1 - b1, s11);
+  }
+  return static_from_sq(S, s11) - static_from_sq(S, s01) - static_from_sq(S, s10) +
+         static_from_sq(S, s00);
+}
+
+// FP32 certification thresholds (sk_gram, include/sigkern_b200.h; the
+// calibration is in DESIGN.md §4):
+//  * realised level-1 noise |k1_fp32 - k1_exact| above the tolerance of its
+//    scale (normalised: 1e-5 sqrt(k_1(x,x) k_1(y,y)); unnormalised: 1e-4 |K|;
+//    self levels: 1e-5 k_1(x,x)) -> the pair's arithmetic is not trusted;
+//  * |K| below CERT_TAU_NORM (normalised) or CERT_TAU_RAW x sum_m |k_m|
+//    (unnormalised; linear kind: CERT_TAU_RAW_LINEAR, whose levels are
+//    inner products of exact increments) -> cancellation beyond what the FP32
+//    level values resolve.
+constexpr double CERT_NOISE = 1e-5;
+constexpr double CERT_NOISE_RAW = 1e-4;
+constexpr double CERT_TAU_NORM = 0.05;
+constexpr double CERT_TAU_RAW = 0.01;
+constexpr double CERT_TAU_RAW_LINEAR = 1e-3;
 
 // ---------------------------------------------------------------------------
 // Level-sum epilogue: kernels.py:586-600 (+ _normalize_levelwise 510-516,
@@ -161,7 +215,7 @@ size_t fast_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int6
 int fast_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
               int64_t ly, int64_t d, int symmetric, const sk_kernel_config &c,
               int64_t row_begin, int64_t row_end, const double *diag_x, const double *diag_y,
-              double *K, int64_t ldk, double *levels, void *ws, size_t ws_bytes,
+              double *K, int64_t ldk, double *levels, float *k1buf, void *ws, size_t ws_bytes,
               cudaStream_t st);
 int fast_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
                      const sk_kernel_config &c, double *out, void *ws, size_t ws_bytes,
@@ -174,7 +228,7 @@ size_t gemm_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int6
 int gemm_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
               int64_t ly, int64_t d, int symmetric, const sk_kernel_config &c,
               int64_t row_begin, int64_t row_end, const double *diag_x, const double *diag_y,
-              double *K, int64_t ldk, double *levels, void *ws, size_t ws_bytes,
+              double *K, int64_t ldk, double *levels, float *k1buf, void *ws, size_t ws_bytes,
               cudaStream_t st);
 int gemm_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
                      const sk_kernel_config &c, double *out, void *ws, size_t ws_bytes,
@@ -216,8 +270,10 @@ int lifted_self_levels(const double *UX, int64_t n, int64_t l, int64_t width,
                        double *out, void *ws, size_t ws_bytes, cudaStream_t st);
 
 // Centring of translation-invariant static kernels on the FP32 paths: the
-// per-channel midrange c = (min + max) / 2 over every point of X (and Y) is
-// subtracted in float64 before the FP32 rounding (k(x, y) = k(x - c, y - c)).
+// per-channel midrange c = (min + max) / 2 over every point of the column role
+// Y (X for K(X) and the self levels) is subtracted from both roles in float64
+// before the FP32 rounding (k(x, y) = k(x - c, y - c)); only pairs with x near
+// some y have a non-negligible point kernel, so Y's spread bounds |x - c| there.
 // The rbf point kernel's norm-expansion exponent carries an absolute FP32
 // error of ~|x'|^2 2^-24, so without it accuracy would depend on the data's
 // distance from the origin. Min and max are exact in any order, so c is
@@ -235,6 +291,44 @@ __device__ __forceinline__ double ord_dec(unsigned long long u) {
 __device__ __forceinline__ double midrange_of(const unsigned long long *mm, int64_t d, int64_t k) {
   return mm ? 0.5 * (ord_dec(mm[k]) + ord_dec(mm[d + k])) : 0.0;
 }
+
+// Float64 fix-ups of the FP32 paths' uncertified results (sk_generic.cu):
+// K entries marked NaN by the Gram epilogue, and self levels whose level 0
+// was marked NaN by the self-level epilogue. The scratch may alias the FP32
+// path's workspace (they run after it in the same stream).
+size_t fixup_workspace_bytes(int64_t lx, int64_t ly, const sk_kernel_config &c);
+int fp64_fixup(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny, int64_t ly,
+               int64_t d, int symmetric, const sk_kernel_config &c, int64_t row_begin,
+               int64_t row_end, const double *diag_x, const double *diag_y, const float *k1buf,
+               double *K, int64_t ldk, double *levels, void *ws, size_t ws_bytes,
+               cudaStream_t st);
+// FP32 level-1 buffer of the certification (rows x ny floats) at the start
+// of an FP32 Gram's workspace; the path's own workspace follows it.
+inline size_t k1buf_bytes(int64_t nx, int64_t ny) {
+  return ((size_t)nx * ny * 4 + 255) & ~(size_t)255;
+}
+int fp64_self_fixup(const double *X, int64_t n, int64_t l, int64_t d, const sk_kernel_config &c,
+                    double *out, void *ws, size_t ws_bytes, cudaStream_t st);
+
+// Order-1 float64 recursion with one CTA per pair (sk_rowscan.cu): the
+// float64 Gram / self levels for rows of >= 32 increments, and the FP32
+// certification's exact-level-1 pass + float64 redo of flagged entries.
+bool rowscan_supported(int64_t lx, int64_t ly, const sk_kernel_config &c);
+size_t rowscan_workspace_bytes(int64_t npairs, int64_t lx, int64_t ly, const sk_kernel_config &c);
+// mode 0 rect, 1 symmetric, 2 self levels (self_out)
+int rowscan_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
+                 int64_t ly, int64_t d, int mode, const sk_kernel_config &c, int64_t row_begin,
+                 int64_t row_end, const double *diag_x, const double *diag_y, double *K,
+                 int64_t ldk, double *levels, double *self_out, void *ws, size_t ws_bytes,
+                 cudaStream_t st);
+size_t cert_workspace_bytes(int64_t lx, int64_t ly, const sk_kernel_config &c);
+int cert_fixup(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny, int64_t ly,
+               int64_t d, int symmetric, const sk_kernel_config &c, int64_t row_begin,
+               int64_t row_end, const double *diag_x, const double *diag_y, const float *k1buf,
+               double *K, int64_t ldk, double *levels, void *ws, size_t ws_bytes,
+               cudaStream_t st);
+int cert_self_fixup(const double *X, int64_t n, int64_t l, int64_t d, const sk_kernel_config &c,
+                    double *out, void *ws, size_t ws_bytes, cudaStream_t st);
 
 // Path selection: 1 fused, 2 GEMM-fed, 0 float64.
 inline int path_of(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {

@@ -63,6 +63,38 @@ __global__ void minmax_kernel(const double *__restrict__ X, int64_t total, int d
   }
 }
 
+// Per-sequence min/max codes (the self-level passes: every sequence centred
+// on its own midrange, so self levels do not depend on the batch): one warp
+// per sequence, mm[s][0..d) min and [d..2d) max.
+__global__ void minmax_seq_kernel(const double *__restrict__ X, int64_t n, int64_t L, int d,
+                                  unsigned long long *__restrict__ mm) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = w0; s < n; s += nw) {
+    const double *seq = X + s * L * d;
+    for (int k = 0; k < d; ++k) {
+      unsigned long long lo = ~0ull, hi = 0ull;
+      for (int64_t r = lane; r < L; r += 32) {
+        const unsigned long long u = ord_enc(seq[r * d + k]);
+        lo = u < lo ? u : lo;
+        hi = u > hi ? u : hi;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o);
+        const unsigned long long b = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = a < lo ? a : lo;
+        hi = b > hi ? b : hi;
+      }
+      if (lane == 0) {
+        mm[s * 2 * d + k] = lo;
+        mm[s * 2 * d + d + k] = hi;
+      }
+    }
+  }
+}
+
 // n-term slot: -|x'|^2/2 for the rbf modes (-1e30 for dummies), 0 for linear
 __device__ __forceinline__ float nterm(int mode, double nrm, bool dummy) {
   if (mode == 1 || mode == 3) return 0.f;
@@ -71,19 +103,21 @@ __device__ __forceinline__ float nterm(int mode, double nrm, bool dummy) {
 
 __global__ void pack_y_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
                               int64_t Lp, int D, double coord_scale, int mode,
-                              const unsigned long long *__restrict__ mm, float *__restrict__ out) {
+                              const unsigned long long *__restrict__ mm, int64_t mm_stride,
+                              float *__restrict__ out) {
   const int YP = y_stride(D);
   const int64_t total = n * Lp;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = t / Lp;
     const double *seq = X + s * L * d;
+    const unsigned long long *ms = mm ? mm + s * mm_stride : nullptr;
     float *dst = out + t * YP;
     double nrm = 0.0;
     bool dummy = false;
     for (int k = 0; k < D; ++k) {
       const float v =
-          (k < d) ? (float)(packed_coord(seq, L, d, t % Lp, k, mode, false, midrange_of(mm, d, k),
+          (k < d) ? (float)(packed_coord(seq, L, d, t % Lp, k, mode, false, midrange_of(ms, d, k),
                                          dummy) * coord_scale)
                   : 0.f;
       dst[k] = v;
@@ -96,7 +130,8 @@ __global__ void pack_y_kernel(const double *__restrict__ X, int64_t n, int64_t L
 
 __global__ void pack_x_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
                               int64_t Lp2, int D, double coord_scale, int mode,
-                              const unsigned long long *__restrict__ mm, float *__restrict__ out) {
+                              const unsigned long long *__restrict__ mm, int64_t mm_stride,
+                              float *__restrict__ out) {
   const int XP = x_stride(D);
   const int64_t total = n * Lp2 * 2;  // one thread per (sequence, row)
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
@@ -105,12 +140,13 @@ __global__ void pack_x_kernel(const double *__restrict__ X, int64_t n, int64_t L
     const int64_t r = t % (2 * Lp2);
     const int half = (int)(r & 1);
     const double *seq = X + s * L * d;
+    const unsigned long long *ms = mm ? mm + s * mm_stride : nullptr;
     float *dst = out + (s * Lp2 + (r >> 1)) * XP;
     double nrm = 0.0;
     bool dummy = false;
     for (int k = 0; k < D; ++k) {
       const float v =
-          (k < d) ? (float)(packed_coord(seq, L, d, r, k, mode, true, midrange_of(mm, d, k), dummy) *
+          (k < d) ? (float)(packed_coord(seq, L, d, r, k, mode, true, midrange_of(ms, d, k), dummy) *
                             coord_scale)
                   : 0.f;
       dst[2 * k + half] = v;
@@ -168,7 +204,10 @@ Plan plan_for(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   // 1e-5 bar, also in a float64-recursion emulation): float64 kernel.
   if (kind == SK_LINEAR && c.order > 1 && c.normalization != SK_NORM_NONE) return pl;
   const int64_t lmin = c.difference ? 2 : 1;  // difference=False: one point is one cell
-  if (d < 1 || d > 16 || lx < lmin || ly < lmin) return pl;
+  // d = 1: one-dimensional paths are cancellation-dominated (level m is
+  // (x_T - x_0)^m/m! from terms of size (sum |dx|)^m/m!); the FP32 sweep
+  // measured 1.7e-5 normalised: float64 kernel
+  if (d < 2 || d > 16 || lx < lmin || ly < lmin) return pl;
   pl.D = d <= 4 ? 4 : (d <= 8 ? 8 : 16);
   const int C = pl.C = columns_per_lane(c.order);
   if (ly <= 32 * C) {
@@ -209,8 +248,10 @@ size_t x_bytes(int64_t n, int64_t lx, const Plan &pl) {
 size_t y_bytes(int64_t n, const Plan &pl) {
   return align256((size_t)n * lyp_of(pl) * y_stride(pl.D) * sizeof(float));
 }
-size_t roles_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t d, const Plan &pl) {
-  return x_bytes(nx, lx, pl) + y_bytes(ny, pl) + carry_bytes(lx, pl) + midrange_bytes(d);
+size_t roles_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t d, const Plan &pl,
+                   bool self_pass = false) {
+  return x_bytes(nx, lx, pl) + y_bytes(ny, pl) + carry_bytes(lx, pl) +
+         midrange_bytes(self_pass ? nx * d : d);
 }
 
 double coord_scale(const sk_kernel_config &c) {
@@ -247,10 +288,11 @@ struct Packed {
   float *carry;
 };
 
+// self_pass: both roles are X and every sequence is centred on its own midrange
 int pack_roles(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
                int64_t ly, int64_t d, const Plan &pl, const sk_kernel_config &c, void *ws,
-               size_t ws_bytes, cudaStream_t st, Packed &out) {
-  const size_t need = roles_bytes(nx, lx, ny, d, pl);
+               size_t ws_bytes, cudaStream_t st, Packed &out, bool self_pass = false) {
+  const size_t need = roles_bytes(nx, lx, ny, d, pl, self_pass);
   if (!ws || ws_bytes < need)
     return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
   const size_t bx = x_bytes(nx, lx, pl), by = y_bytes(ny, pl);
@@ -262,20 +304,33 @@ int pack_roles(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t
   const int incr = pl.nodiff ? (pl.linear ? 3 : 2) : (pl.linear ? 1 : 0);
   // translation-invariant kinds: midrange centring (sk_common.cuh)
   const unsigned long long *mm = nullptr;
+  int64_t mm_stride = 0;
   if (!pl.linear) {
-    const int rc = midrange(X, nx, lx, Y == X ? nullptr : Y, ny, ly, d,
-                            (unsigned long long *)((char *)ws + bx + by + carry_bytes(lx, pl)),
-                            &mm, st);
-    if (rc) return rc;
+    unsigned long long *mmb =
+        (unsigned long long *)((char *)ws + bx + by + carry_bytes(lx, pl));
+    if (self_pass) {
+      // self levels: each sequence on its own midrange (batch-independent)
+      if (d <= 1024 && nx > 0) {
+        minmax_seq_kernel<<<pack_blocks(nx * 32), 256, 0, st>>>(X, nx, lx, (int)d, mmb);
+        SK_CHECK_LAUNCH();
+        mm = mmb;
+        mm_stride = 2 * d;
+      }
+    } else {
+      // Gram: centre of the column role only, so rows of K(X, Y) are the Gram
+      // of those rows bit for bit
+      const int rc = midrange(Y, ny, ly, nullptr, 0, 0, d, mmb, &mm, st);
+      if (rc) return rc;
+    }
   }
   if (nx > 0) {
     pack_x_kernel<<<pack_blocks(nx * lx2 * 2), 256, 0, st>>>(X, nx, lx, d, lx2, pl.D, cs, incr,
-                                                             mm, xsb);
+                                                             mm, mm_stride, xsb);
     SK_CHECK_LAUNCH();
   }
   if (ny > 0) {
     pack_y_kernel<<<pack_blocks(ny * lyp), 256, 0, st>>>(Y, ny, ly, d, lyp, pl.D, cs, incr,
-                                                         mm, ysb);
+                                                         mm, mm_stride, ysb);
     SK_CHECK_LAUNCH();
   }
   out.xs = xsb;
@@ -316,7 +371,7 @@ size_t fast_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int6
   using namespace fast;
   const Plan pl = ny > 0 ? plan_for(lx, ly, d, c) : plan_for(lx, lx, d, c);
   if (!pl.ok) return 0;
-  return roles_bytes(nx, lx, ny > 0 ? ny : nx, d, pl);
+  return roles_bytes(nx, lx, ny > 0 ? ny : nx, d, pl, ny <= 0);
 }
 
 size_t midrange_bytes(int64_t d) { return (2 * (size_t)d * 8 + 255) & ~(size_t)255; }
@@ -346,7 +401,7 @@ int midrange(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t n
 int fast_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
               int64_t ly, int64_t d, int symmetric, const sk_kernel_config &c,
               int64_t row_begin, int64_t row_end, const double *diag_x, const double *diag_y,
-              double *K, int64_t ldk, double *levels, void *ws, size_t ws_bytes,
+              double *K, int64_t ldk, double *levels, float *k1buf, void *ws, size_t ws_bytes,
               cudaStream_t st) {
   using namespace fast;
   if (symmetric) {
@@ -379,6 +434,8 @@ int fast_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t 
   P.K = K;
   P.ldk = ldk;
   P.levels = levels;
+  P.cert = 1;
+  P.k1buf = k1buf;
   return launch(P, pl, c.n_levels, c.order, st);
 }
 
@@ -390,7 +447,7 @@ int fast_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
   if (!pl.ok) return fail(SK_ERR_UNSUPPORTED, "fast path does not cover this configuration");
   if (n <= 0) return SK_OK;
   Packed pk{};
-  int rc = pack_roles(X, n, l, X, n, l, d, pl, c, ws, ws_bytes, st, pk);
+  int rc = pack_roles(X, n, l, X, n, l, d, pl, c, ws, ws_bytes, st, pk, true);
   if (rc) return rc;
   // each CTA evaluates its segments' y against the same sequences as x and
   // keeps the diagonal: the same kernel and arithmetic as the Gram's diagonal

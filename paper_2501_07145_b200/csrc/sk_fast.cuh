@@ -104,6 +104,11 @@ struct Params {
   // S + (x - x_blk0) * s_xstride + y * s_ystride + r * s_ld
   const float *S;
   int64_t s_ld, s_xstride, s_ystride, x_blk0;
+  // FP32 certification (write_pair; sk_gram in include/sigkern_b200.h):
+  // cert = 1 NaN-marks uncertified entries for the float64 fix-up; k1buf
+  // (rows x ny floats, may be null) receives each entry's FP32 level 1
+  int cert;
+  float *k1buf;
 };
 
 typedef unsigned long long u64;
@@ -184,6 +189,10 @@ __device__ __forceinline__ void stage_sequence(float *dst, const float *src, int
 
 // Level values of pair (i, j) -> per-level output and/or normalised K entry.
 // ls = k_1..k_{M-1} (float chain totals), kout = k_M.
+// Certification (sk_gram): an entry that is non-finite or small against its
+// scale (|K| < CERT_TAU_NORM normalised, |K| < CERT_TAU_RAW sum_m |k_m|
+// unnormalised) is written as NaN for the float64 fix-up; the FP32 level 1
+// goes to `k1buf` for the fix-up pass's exact-level-1 check.
 template <int M>
 __device__ __forceinline__ void write_pair(const Params &P, int64_t i, int64_t j,
                                            const float *ls, float kout) {
@@ -202,6 +211,13 @@ __device__ __forceinline__ void write_pair(const Params &P, int64_t i, int64_t j
   if (P.symmetric && i > j) return;
   const int64_t row = P.symmetric ? i : i - P.row_begin;
   const bool mirror = P.symmetric && i != j;
+  const double *dx = P.diag_x ? P.diag_x + i * (M + 1) : nullptr;
+  const double *dy = P.diag_y ? P.diag_y + j * (M + 1) : nullptr;
+  const bool self = P.symmetric && i == j && dx;
+  if (self) {  // K(X)'s diagonal from the self levels: normalised diagonals exactly 1
+#pragma unroll
+    for (int m = 0; m <= M; ++m) lv[m] = dx[m];
+  }
   if (P.levels) {
 #pragma unroll
     for (int m = 0; m <= M; ++m) P.levels[(row * P.ldk + j) * (M + 1) + m] = lv[m];
@@ -211,10 +227,20 @@ __device__ __forceinline__ void write_pair(const Params &P, int64_t i, int64_t j
     }
   }
   if (P.K) {
-    const double v = finish_entry(lv, M, P.norm, P.diag_x ? P.diag_x + i * (M + 1) : nullptr,
-                                  P.diag_y ? P.diag_y + j * (M + 1) : nullptr);
+    double v = finish_entry(lv, M, P.norm, dx, dy);
+    if (P.cert && !self) {
+      double lim = CERT_TAU_NORM;
+      if (P.norm == SK_NORM_NONE) {
+        lim = 0.0;
+#pragma unroll
+        for (int m = 0; m <= M; ++m) lim += fabs(lv[m]);
+        lim *= P.static_kind == SK_LINEAR ? CERT_TAU_RAW_LINEAR : CERT_TAU_RAW;
+      }
+      if (!(fabs(v) >= lim) || isinf(v)) v = __longlong_as_double(0x7ff8000000000000ll);
+    }
     P.K[row * P.ldk + j] = v;
     if (mirror) P.K[j * P.ldk + i] = v;
+    if (P.k1buf) P.k1buf[row * P.ny + j] = self ? 0.f : (M >= 1 ? (float)lv[1] : 0.f);
   }
 }
 
@@ -858,13 +884,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) gram_kernel(const Params P) {
 //  pair), and rows/columns beyond L are dummies whose point kernel is 0 (rbf:
 //  n-term -1e30, so exp2 underflows to 0; linear: zero coordinates).
 //  mm: midrange codes (sk_common.cuh) subtracted from the points in modes 0
-//  and 2, or null.
+//  and 2, or null; mm_stride: 0 (one centre) or 2d (per sequence).
 __global__ void pack_y_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
                               int64_t Lp, int D, double coord_scale, int mode,
-                              const unsigned long long *__restrict__ mm, float *__restrict__ out);
+                              const unsigned long long *__restrict__ mm, int64_t mm_stride,
+                              float *__restrict__ out);
 __global__ void pack_x_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
                               int64_t Lp2, int D, double coord_scale, int mode,
-                              const unsigned long long *__restrict__ mm, float *__restrict__ out);
+                              const unsigned long long *__restrict__ mm, int64_t mm_stride,
+                              float *__restrict__ out);
+__global__ void minmax_seq_kernel(const double *__restrict__ X, int64_t n, int64_t L, int d,
+                                  unsigned long long *__restrict__ mm);
 
 int launch_d4(const Params &, int M, int order, int variant, size_t smem, cudaStream_t st);
 int launch_d8(const Params &, int M, int order, int variant, size_t smem, cudaStream_t st);

@@ -149,7 +149,7 @@ __device__ __forceinline__ void put_split(float *hi, float *lo, int k, float v) 
 
 __global__ void pack_rows_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
                                  int64_t rows, int K, double coord_scale, int mode,
-                                 const unsigned long long *__restrict__ mm,
+                                 const unsigned long long *__restrict__ mm, int64_t mm_stride,
                                  float *__restrict__ hi, float *__restrict__ lo) {
   const int64_t total = n * rows;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
@@ -162,7 +162,7 @@ __global__ void pack_rows_kernel(const double *__restrict__ X, int64_t n, int64_
     for (int k = 0; k < d; ++k) {
       double v = seq[pt * d + k];
       if (mode == 2) v = (r >= 1 && r < L) ? v - seq[(pt - 1) * d + k] : 0.0;
-      else v -= midrange_of(mm, d, k);  // rbf: centring (sk_common.cuh)
+      else v -= midrange_of(mm ? mm + s * mm_stride : nullptr, d, k);  // rbf: centring
       const float f = (float)(v * coord_scale);
       put_split(dh, dl, k, f);
       nrm += (double)f * (double)f;
@@ -203,7 +203,7 @@ Plan plan_for(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   if (!fast::fast_orders_supported(c.n_levels, c.order)) return pl;
   if (c.order != 1 && c.order != c.n_levels) return pl;  // DP instantiated for p = 1 and p = M
   if (kind == SK_LINEAR && c.order > 1 && c.normalization != SK_NORM_NONE) return pl;
-  if (d < 1 || lx < 2 || ly < 2) return pl;
+  if (d < 2 || lx < 2 || ly < 2) return pl;  // d = 1: float64 (see sk_fast.cu plan_for)
   pl.linear = kind == SK_LINEAR;
   pl.K = (int)((pl.linear ? d : d + 2) + 3) / 4 * 4;
   const int C = pl.C = fast::columns_per_lane(c.order);
@@ -257,7 +257,8 @@ size_t gram_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t d, const Plan &pl)
 
 size_t self_bytes(int64_t n, int64_t l, int64_t d, const Plan &pl) {
   return operand_bytes(n, rows_x(l), pl) + operand_bytes(n, cols_y(pl), pl) +
-         align256((size_t)n * rows_x(l) * cols_y(pl) * 4) + carry_bytes(l, pl) + midrange_bytes(d);
+         align256((size_t)n * rows_x(l) * cols_y(pl) * 4) + carry_bytes(l, pl) +
+         midrange_bytes(n * d);  // per-sequence centres
 }
 
 unsigned pack_blocks(int64_t total) {
@@ -277,12 +278,12 @@ Operand carve(void *&cursor, int64_t n, int64_t rows, const Plan &pl) {
 }
 
 int pack(const double *X, int64_t n, int64_t L, int64_t d, int64_t rows, const Plan &pl,
-         const sk_kernel_config &c, bool xrole, const unsigned long long *mm, Operand out,
-         cudaStream_t st) {
+         const sk_kernel_config &c, bool xrole, const unsigned long long *mm, int64_t mm_stride,
+         Operand out, cudaStream_t st) {
   if (n <= 0) return SK_OK;
   const int mode = pl.linear ? 2 : (xrole ? 0 : 1);
   pack_rows_kernel<<<pack_blocks(n * rows), 256, 0, st>>>(X, n, L, d, rows, pl.K, coord_scale(c),
-                                                          mode, mm, out.hi, out.lo);
+                                                          mode, mm, mm_stride, out.hi, out.lo);
   SK_CHECK_LAUNCH();
   return SK_OK;
 }
@@ -343,6 +344,7 @@ Params base_params(const Plan &pl, int64_t lx, float *carry) {
   P.nhp = pl.nhp;
   P.carry = carry;
   P.max_ctas = sm_count();
+  P.static_kind = pl.linear ? SK_LINEAR : SK_RBF;  // certification thresholds (write_pair)
   return P;
 }
 
@@ -368,7 +370,7 @@ size_t gemm_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int6
 int gemm_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
               int64_t ly, int64_t d, int symmetric, const sk_kernel_config &c,
               int64_t row_begin, int64_t row_end, const double *diag_x, const double *diag_y,
-              double *K, int64_t ldk, double *levels, void *ws, size_t ws_bytes,
+              double *K, int64_t ldk, double *levels, float *k1buf, void *ws, size_t ws_bytes,
               cudaStream_t st) {
   using namespace gemm;
   if (symmetric) {
@@ -389,12 +391,12 @@ int gemm_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t 
   float *carry = (float *)((char *)sblk + align256((size_t)bx * rx * ny * cy * 4));
   const unsigned long long *mm = nullptr;
   if (!pl.linear) {
-    const int r = midrange(X, nx, lx, symmetric ? nullptr : Y, ny, ly, d,
+    const int r = midrange(Y, ny, ly, nullptr, 0, 0, d,  // column role (see sk_fast.cu)
                            (unsigned long long *)((char *)carry + carry_bytes(lx, pl)), &mm, st);
     if (r) return r;
   }
-  int rc = pack(X, nx, lx, d, rx, pl, c, true, mm, xg, st);
-  if (!rc) rc = pack(Y, ny, ly, d, cy, pl, c, false, mm, yg, st);
+  int rc = pack(X, nx, lx, d, rx, pl, c, true, mm, 0, xg, st);
+  if (!rc) rc = pack(Y, ny, ly, d, cy, pl, c, false, mm, 0, yg, st);
   if (rc) return rc;
   if (row_end <= row_begin || ny <= 0) return SK_OK;
   Params P = base_params(pl, lx, carry);
@@ -408,6 +410,8 @@ int gemm_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t 
   P.K = K;
   P.ldk = ldk;
   P.levels = levels;
+  P.cert = 1;
+  P.k1buf = k1buf;
   P.S = sblk;
   P.s_ld = ny * cy;
   P.s_xstride = rx * ny * cy;
@@ -429,6 +433,7 @@ int gemm_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t 
     // symmetric K(X): the kernel writes rows >= row_begin of the full matrix;
     // cross: rows relative to the caller's row_begin
     if (!symmetric) {
+      P.k1buf = k1buf ? k1buf + (b0 - row_begin) * ny : nullptr;
       P.K = K ? K + (b0 - row_begin) * ldk : nullptr;
       P.levels = levels ? levels + (b0 - row_begin) * ldk * (c.n_levels + 1) : nullptr;
       P.row_begin = b0;  // write_pair subtracts row_begin
@@ -456,14 +461,14 @@ int gemm_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
   const Operand yg = carve(cur, n, cy, pl);
   float *sb = (float *)cur;
   float *carry = (float *)((char *)sb + align256((size_t)n * rx * cy * 4));
-  const unsigned long long *mm = nullptr;
-  if (!pl.linear) {
-    const int r = midrange(X, n, l, nullptr, 0, 0, d,
-                           (unsigned long long *)((char *)carry + carry_bytes(l, pl)), &mm, st);
-    if (r) return r;
+  unsigned long long *mm = nullptr;
+  if (!pl.linear && d <= 1024) {  // self levels: each sequence on its own midrange
+    mm = (unsigned long long *)((char *)carry + carry_bytes(l, pl));
+    fast::minmax_seq_kernel<<<pack_blocks(n * 32), 256, 0, st>>>(X, n, l, (int)d, mm);
+    SK_CHECK_LAUNCH();
   }
-  int rc = pack(X, n, l, d, rx, pl, c, true, mm, xg, st);
-  if (!rc) rc = pack(X, n, l, d, cy, pl, c, false, mm, yg, st);
+  int rc = pack(X, n, l, d, rx, pl, c, true, mm, 2 * d, xg, st);
+  if (!rc) rc = pack(X, n, l, d, cy, pl, c, false, mm, 2 * d, yg, st);
   if (rc) return rc;
   // per-sequence cell matrices (pairs (i, i)): batched GEMM, [n][rx][cy]
   rc = tc_gemm_3xtf32(yg.hi, yg.lo, cy, xg.hi, xg.lo, rx, pl.K, sb, cy, n, rx * cy, st);

@@ -70,21 +70,16 @@ __device__ inline double lifted_dot(const GenParams &P, int h, const double *x, 
   return acc;
 }
 
-__global__ void __launch_bounds__(GEN_THREADS) generic_levels_kernel(GenParams P) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= P.count) return;
-  const int64_t g = P.g0 + t;
-  int64_t i, j;
-  pair_of(P, g, i, j);
+// Level values of pair (i, j) (pair id g) into out[0..M]; this thread's
+// column state is scratch slot t of CH interleaved slots.
+__device__ void pair_levels(const GenParams &P, int64_t g, int64_t i, int64_t j, int64_t t,
+                            int64_t CH, double *out) {
   const int M = P.M;
-  double *out = P.lv + t * (M + 1);
   out[0] = 1.0;
   for (int m = 1; m <= M; ++m) out[m] = 0.0;
-  if (P.mode == 1 && j < i) return;  // lower triangle of a symmetric Gram is mirrored
   const int64_t T1 = P.t1, T2 = P.t2;
   if (M == 0 || T1 <= 0 || T2 <= 0) return;
   const int p = P.p;
-  const int64_t CH = P.count;
 
   // workspace slots: colC[(m-1)*T2 + j] m=1..M-1, colSY[((m-1)*(p-1)+r)*T2 + j], Gprev[ly]
   double *colC = P.scratch + t;
@@ -224,6 +219,115 @@ __global__ void __launch_bounds__(GEN_THREADS) generic_levels_kernel(GenParams P
   for (int m = 1; m <= M; ++m) out[m] = lsum[m];
 }
 
+__global__ void __launch_bounds__(GEN_THREADS) generic_levels_kernel(GenParams P) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= P.count) return;
+  const int64_t g = P.g0 + t;
+  int64_t i, j;
+  pair_of(P, g, i, j);
+  double *out = P.lv + t * (P.M + 1);
+  if (P.mode == 1 && j < i) {  // lower triangle of a symmetric Gram is mirrored
+    out[0] = 1.0;
+    for (int m = 1; m <= P.M; ++m) out[m] = 0.0;
+    return;
+  }
+  pair_levels(P, g, i, j, t, P.count, out);
+}
+
+// FP32 certification pass (sk_common.cuh, fp64_fixup), after the FP32 Gram
+// kernel in the same stream, one grid-stride scan over the row range of K:
+//  * an entry the FP32 epilogue marked NaN (non-finite, or small against its
+//    scale) is recomputed in float64 — the pair's levels and, when
+//    normalised, both self levels — and written with its mirror (K(X)) and
+//    its per-level output (if requested);
+//  * otherwise (difference=True) the pair's exact level 1 (exact_level1, the
+//    telescoped increments) is compared with the FP32 one the epilogue left
+//    in k1buf: a deviation above CERT_NOISE of the entry's scale marks the
+//    pair's arithmetic as noisy (float64 recompute as above), else the entry
+//    is corrected to the exact level 1.
+// One scratch slot per thread: no list, no host synchronisation.
+struct FixupArgs {
+  GenParams pair;   // mode 0 / 1 geometry of the Gram (X rows, Y columns)
+  GenParams selfx;  // paired geometry over X (self levels of row sequences)
+  GenParams selfy;  // ... over Y
+  int norm;
+  double *K;
+  int64_t ldk;
+  double *levels;
+  int64_t rows;     // rows of the range
+  const float *k1buf;  // FP32 level 1 per entry [row][ny], or null
+  const double *diag_x, *diag_y;
+};
+
+__device__ inline void put_entry(const FixupArgs &A, int64_t row, int64_t i, int64_t j, bool sym,
+                                 double v) {
+  A.K[row * A.ldk + j] = v;
+  if (sym && j != i) A.K[j * A.ldk + i] = v;
+}
+
+__global__ void __launch_bounds__(GEN_THREADS) fixup_kernel(FixupArgs A) {
+  const GenParams &P = A.pair;
+  const int M = P.M;
+  const bool sym = P.mode == 1;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = A.rows * P.ny;
+  double lv[GEN_MAX_LEVELS + 1], dx[GEN_MAX_LEVELS + 1], dy[GEN_MAX_LEVELS + 1];
+  for (int64_t e = t; e < total; e += nthr) {
+    const int64_t r = e / P.ny, j = e % P.ny;
+    const int64_t i = P.row_begin + r;
+    const int64_t row = sym ? i : r;
+    if (sym && j < i) continue;
+    double v = A.K[row * A.ldk + j];
+    bool redo = isnan(v);
+    if (!redo && A.k1buf && P.difference && M >= 1 && !(sym && i == j)) {
+      const double k1e = exact_level1(P.S, P.X + i * P.lx * P.d, P.lx, P.Y + j * P.ly * P.d, P.ly,
+                                      (int)P.d);
+      const double delta = k1e - (double)A.k1buf[row * P.ny + j];
+      double scale = CERT_NOISE_RAW / CERT_NOISE * fabs(v), corr = delta;
+      if (A.norm != SK_NORM_NONE) {
+        const double *px = A.diag_x + i * (M + 1), *py = A.diag_y + j * (M + 1);
+        scale = sqrt(fabs(px[1] * py[1]));
+        if (A.norm == SK_NORM_LEVELWISE) {
+          const double den = sqrt((px[1] > 0.0 ? px[1] : 0.0) * (py[1] > 0.0 ? py[1] : 0.0));
+          corr = den > 0.0 ? delta / den / (double)(M + 1) : 0.0;
+        } else {
+          double sx = 0.0, sy = 0.0;
+          for (int m = 0; m <= M; ++m) {
+            sx += px[m];
+            sy += py[m];
+          }
+          corr = delta / sqrt(sx * sy);
+        }
+      }
+      if (fabs(delta) > CERT_NOISE * scale) {
+        redo = true;
+      } else {
+        put_entry(A, row, i, j, sym, v + corr);
+        if (A.levels) {
+          A.levels[(row * A.ldk + j) * (M + 1) + 1] = k1e;
+          if (sym && j != i) A.levels[(j * A.ldk + i) * (M + 1) + 1] = k1e;
+        }
+      }
+    }
+    if (!redo) continue;
+    pair_levels(P, 0, i, j, t, nthr, lv);
+    const double *px = nullptr, *py = nullptr;
+    if (A.norm != SK_NORM_NONE) {
+      pair_levels(A.selfx, 0, i, i, t, nthr, dx);
+      pair_levels(A.selfy, 0, j, j, t, nthr, dy);
+      px = dx;
+      py = dy;
+    }
+    put_entry(A, row, i, j, sym, finish_entry(lv, M, A.norm, px, py));
+    if (A.levels) {
+      for (int m = 0; m <= M; ++m) A.levels[(row * A.ldk + j) * (M + 1) + m] = lv[m];
+      if (sym && j != i)
+        for (int m = 0; m <= M; ++m) A.levels[(j * A.ldk + i) * (M + 1) + m] = lv[m];
+    }
+  }
+}
+
 // Normalisation / level-sum epilogue for a chunk of pairs (kernels.py:586-600).
 __global__ void generic_finish_kernel(GenParams P, int norm, const double *diag_x,
                                       const double *diag_y, double *K, int64_t ldk,
@@ -356,6 +460,120 @@ int generic_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
   if (n <= 0) return SK_OK;
   return run_chunks(P, n, SK_NORM_NONE, nullptr, nullptr, nullptr, 0, nullptr, out, ws,
                     ws_bytes, st);
+}
+
+namespace {
+// Self-level fix-up: sequences whose level 0 the FP32 self-level epilogue
+// marked NaN are recomputed in float64 (one thread per flagged sequence of a
+// grid-stride scan).
+// Self levels of the FP32 paths: level 1 -> its exact telescoped value;
+// a sequence whose FP32 level 1 deviates from it by more than CERT_NOISE
+// relative, or with a negative or non-finite level (self levels are >= 0),
+// is recomputed in float64.
+__global__ void __launch_bounds__(GEN_THREADS) self_fixup_kernel(GenParams P, int64_t n,
+                                                                 double *out) {
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int M = P.M;
+  double lv[GEN_MAX_LEVELS + 1];
+  for (int64_t i = t; i < n; i += nthr) {
+    double *o = out + i * (M + 1);
+    bool redo = false;
+    for (int m = 1; m <= M; ++m) redo |= !(o[m] >= 0.0) || isinf(o[m]);
+    if (!redo && P.difference && M >= 1) {
+      const double *x = P.X + i * P.lx * P.d;
+      const double k1e = exact_level1(P.S, x, P.lx, x, P.lx, (int)P.d);
+      if (fabs(o[1] - k1e) > CERT_NOISE * fabs(k1e))
+        redo = true;
+      else
+        o[1] = k1e;
+    }
+    if (!redo) continue;
+    pair_levels(P, 0, i, i, t, nthr, lv);
+    for (int m = 0; m <= M; ++m) o[m] = lv[m];
+  }
+}
+}  // namespace
+
+namespace {
+constexpr int64_t FIXUP_THREADS_MAX = 148 * 2 * GEN_THREADS;
+constexpr int64_t FIXUP_SCRATCH_BUDGET = 96ll << 20;
+
+int64_t fixup_threads(int64_t lx, int64_t ly, const sk_kernel_config &c) {
+  const int M = c.n_levels;
+  const int p = std::max(1, std::min(c.order, std::max(M, 1)));
+  const int64_t L = std::max(lx, ly);
+  const int64_t t = c.difference ? std::max<int64_t>(L - 1, 0) : L;
+  const int64_t per = scratch_slots(t, L, M, p) * 8;
+  const int64_t n = std::min<int64_t>(FIXUP_THREADS_MAX, FIXUP_SCRATCH_BUDGET / per);
+  return std::max<int64_t>(GEN_THREADS, n / GEN_THREADS * GEN_THREADS);
+}
+}  // namespace
+
+size_t fixup_workspace_bytes(int64_t lx, int64_t ly, const sk_kernel_config &c) {
+  const int M = c.n_levels;
+  const int p = std::max(1, std::min(c.order, std::max(M, 1)));
+  const int64_t L = std::max(lx, ly);
+  const int64_t t = c.difference ? std::max<int64_t>(L - 1, 0) : L;
+  return (size_t)fixup_threads(lx, ly, c) * scratch_slots(t, L, M, p) * 8;
+}
+
+int fp64_fixup(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny, int64_t ly,
+               int64_t d, int symmetric, const sk_kernel_config &c, int64_t row_begin,
+               int64_t row_end, const double *diag_x, const double *diag_y, const float *k1buf,
+               double *K, int64_t ldk, double *levels, void *ws, size_t ws_bytes,
+               cudaStream_t st) {
+  if (!K || row_end <= row_begin || ny <= 0 || nx <= 0) return SK_OK;
+  if (symmetric) {
+    Y = X;
+    ny = nx;
+    ly = lx;
+  }
+  if (c.n_levels > GEN_MAX_LEVELS || c.order > GEN_MAX_ORDER)
+    return fail(SK_ERR_UNSUPPORTED, "fix-up: n_levels/order beyond the float64 kernel");
+  const size_t need = fixup_workspace_bytes(lx, ly, c);
+  if (!ws || ws_bytes < need)
+    return fail(SK_ERR_WORKSPACE, "workspace too small for the fix-up: need " + std::to_string(need));
+  FixupArgs A{};
+  A.pair = base_params(X, nx, lx, Y, ny, ly, d, c);
+  A.pair.mode = symmetric ? 1 : 0;
+  A.pair.row_begin = row_begin;
+  A.pair.scratch = (double *)ws;
+  A.selfx = base_params(X, nx, lx, X, nx, lx, d, c);
+  A.selfx.mode = 2;
+  A.selfx.scratch = (double *)ws;
+  A.selfy = base_params(Y, ny, ly, Y, ny, ly, d, c);
+  A.selfy.mode = 2;
+  A.selfy.scratch = (double *)ws;
+  A.norm = c.normalization;
+  A.K = K;
+  A.ldk = ldk;
+  A.levels = levels;
+  A.rows = row_end - row_begin;
+  A.k1buf = k1buf;
+  A.diag_x = diag_x;
+  A.diag_y = symmetric ? diag_x : diag_y;
+  const int64_t nthr = fixup_threads(lx, ly, c);
+  fixup_kernel<<<(unsigned)(nthr / GEN_THREADS), GEN_THREADS, 0, st>>>(A);
+  SK_CHECK_LAUNCH();
+  return SK_OK;
+}
+
+int fp64_self_fixup(const double *X, int64_t n, int64_t l, int64_t d, const sk_kernel_config &c,
+                    double *out, void *ws, size_t ws_bytes, cudaStream_t st) {
+  if (n <= 0 || !out) return SK_OK;
+  if (c.n_levels > GEN_MAX_LEVELS || c.order > GEN_MAX_ORDER)
+    return fail(SK_ERR_UNSUPPORTED, "fix-up: n_levels/order beyond the float64 kernel");
+  const size_t need = fixup_workspace_bytes(l, l, c);
+  if (!ws || ws_bytes < need)
+    return fail(SK_ERR_WORKSPACE, "workspace too small for the fix-up: need " + std::to_string(need));
+  GenParams P = base_params(X, n, l, X, n, l, d, c);
+  P.mode = 2;
+  P.scratch = (double *)ws;
+  const int64_t nthr = std::min<int64_t>(fixup_threads(l, l, c), (n + GEN_THREADS - 1) / GEN_THREADS * GEN_THREADS);
+  self_fixup_kernel<<<(unsigned)(nthr / GEN_THREADS), GEN_THREADS, 0, st>>>(P, n, out);
+  SK_CHECK_LAUNCH();
+  return SK_OK;
 }
 
 // --- rfsf_exact_gram's lifted level Grams (features.py:397-443), float64 ---------

@@ -1,0 +1,495 @@
+// Float64 level recursion at order p = 1 with one CTA per sequence pair.
+//
+// The reference's recursion (kernels.py:174-199 at p = 1: R_m = A * S(R_{m-1}),
+// S the 2-D exclusive prefix) is streamed row by row over the pair's T1 x T2
+// increment grid, the columns split into contiguous blocks over the CTA's 256
+// threads. Per row every thread forms its cells' increments from the float64
+// point kernel (the left-boundary point-kernel value comes from the previous
+// thread: shuffle, or shared memory across warps), takes the exclusive row
+// prefix of every level's column accumulators with one block-wide scan of
+// M-1 values, and updates the level sums. Column accumulators live in a
+// per-CTA global scratch slice (L2-resident, (M-1) x T2 doubles).
+//
+// This replaces the thread-per-pair float64 kernel (sk_generic.cu) where one
+// pair must be fast: the certification fix-ups of the FP32 paths (a flagged
+// c3 entry costs ~0.6 s on the thread-per-pair kernel, a c5 entry ~17 s,
+// because a lone thread walks the grid through dependent global-memory state)
+// and the order-1 float64 Gram.
+#include <algorithm>
+
+#include "sk_common.cuh"
+
+namespace sk {
+namespace rowscan {
+
+constexpr int RT = 256;            // threads per CTA
+constexpr int NW = RT / 32;
+constexpr int CMAX = 16;           // columns per thread: T2 <= 4096
+constexpr int VMAX = GEN_MAX_LEVELS - 1;  // scanned levels (1..M-1)
+
+struct Geo {
+  const double *X, *Y;
+  int64_t nx, lx, ny, ly, d;
+  StaticF64 S;
+  int M, difference;
+};
+
+// Block-wide exclusive prefix of nv values per thread (in place); every thread
+// must call it. sm: NW * VMAX doubles.
+__device__ __forceinline__ void block_excl_scan(double (&v)[VMAX], int nv, double *sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double inc[VMAX];
+#pragma unroll
+  for (int k = 0; k < VMAX; ++k) inc[k] = v[k];
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+    for (int k = 0; k < VMAX; ++k) {
+      if (k < nv) {
+        const double u = __shfl_up_sync(0xffffffffu, inc[k], o);
+        if (lane >= o) inc[k] += u;
+      }
+    }
+  }
+  if (lane == 31)
+    for (int k = 0; k < nv; ++k) sm[warp * VMAX + k] = inc[k];
+  __syncthreads();
+  for (int k = 0; k < nv; ++k) {
+    double off = 0.0;
+    for (int w = 0; w < warp; ++w) off += sm[w * VMAX + k];
+    v[k] = off + inc[k] - v[k];
+  }
+  __syncthreads();  // sm reusable
+}
+
+// Block-wide sum of v[0..n) into out[0..n) (thread 0). sm: NW * (VMAX + 1).
+__device__ __forceinline__ void block_sum(const double *v, int n, double *sm, double *out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = 0; k < n; ++k) {
+    double s = v[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) sm[warp * (VMAX + 1) + k] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int k = 0; k < n; ++k) {
+      double s = 0.0;
+      for (int w = 0; w < NW; ++w) s += sm[w * (VMAX + 1) + k];
+      out[k] = s;
+    }
+  __syncthreads();
+}
+
+// Level values k_0..k_M of the pair (xs: lx points, ys: ly points) into
+// lv_out[0..M] (shared memory, written by thread 0; visible after return).
+// colacc: this CTA's scratch, (M-1) * T2 doubles. All threads call it.
+__device__ void cta_pair_levels(const Geo &G, const double *__restrict__ xs, int64_t lx,
+                                const double *__restrict__ ys, int64_t ly,
+                                double *__restrict__ colacc, double *sm, double *lv_out) {
+  const int M = G.M, d = (int)G.d;
+  const int64_t T1 = G.difference ? lx - 1 : lx, T2 = G.difference ? ly - 1 : ly;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (M == 0 || T1 <= 0 || T2 <= 0) {
+    if (t == 0) {
+      lv_out[0] = 1.0;
+      for (int m = 1; m <= M; ++m) lv_out[m] = 0.0;
+    }
+    __syncthreads();
+    return;
+  }
+  const int C = (int)((T2 + RT - 1) / RT);
+  const int64_t c0 = std::min<int64_t>((int64_t)t * C, T2);
+  const int n = (int)(std::min<int64_t>(c0 + C, T2) - c0);  // own cells of a row
+  const int NV = M - 1;
+  for (int m = 0; m < NV; ++m)
+    for (int k = 0; k < n; ++k) colacc[m * T2 + c0 + k] = 0.0;
+  // point-kernel values of the previous row at columns c0 .. c0 + n (difference)
+  double gp[CMAX + 1];
+  if (G.difference)
+    for (int k = 0; k <= n; ++k) gp[k] = static_eval_f64(G.S, xs, ys + (c0 + k) * d, d);
+  double lsum[GEN_MAX_LEVELS];
+  for (int m = 0; m < M; ++m) lsum[m] = 0.0;
+  double *smb = sm + NW * VMAX;  // warp-boundary point-kernel values
+  for (int64_t r = 0; r < T1; ++r) {
+    double a[CMAX];
+    if (G.difference) {
+      const double *xa = xs + (r + 1) * d;
+      // G(r+1, c0 + k) for k = 1..n here; k = 0 from the previous thread
+      double g[CMAX + 1];
+      for (int k = 1; k <= n; ++k) g[k] = static_eval_f64(G.S, xa, ys + (c0 + k) * d, d);
+      const double last = n > 0 ? g[n] : 0.0;
+      const double up = __shfl_up_sync(0xffffffffu, last, 1);
+      if (lane == 31) smb[warp] = last;
+      __syncthreads();
+      if (t == 0)
+        g[0] = static_eval_f64(G.S, xa, ys, d);
+      else
+        g[0] = lane == 0 ? smb[warp - 1] : up;
+      // kernels.py:281: G[1:,1:] - G[:-1,1:] - G[1:,:-1] + G[:-1,:-1]
+      for (int k = 0; k < n; ++k) a[k] = g[k + 1] - gp[k + 1] - g[k] + gp[k];
+      for (int k = 0; k <= n; ++k) gp[k] = g[k];
+    } else {
+      for (int k = 0; k < n; ++k)
+        a[k] = static_eval_f64(G.S, xs + r * d, ys + (c0 + k) * d, d);
+    }
+    // exclusive row prefix of the column accumulators (old values), levels 1..M-1
+    double pre[VMAX];
+    for (int m = 0; m < VMAX; ++m) pre[m] = 0.0;
+    for (int m = 0; m < NV; ++m)
+      for (int k = 0; k < n; ++k) pre[m] += colacc[m * T2 + c0 + k];
+    block_excl_scan(pre, NV, sm);
+    for (int k = 0; k < n; ++k) {
+      const int64_t c = c0 + k;
+      double Rprev = a[k];  // R_1
+      lsum[0] += Rprev;
+      for (int m = 1; m < M; ++m) {  // R_{m+1} = A * S_m
+        const double R = a[k] * pre[m - 1];
+        lsum[m] += R;
+        double &acc = colacc[(m - 1) * T2 + c];
+        const double old = acc;
+        pre[m - 1] += old;
+        acc = old + Rprev;
+        Rprev = R;
+      }
+    }
+  }
+  block_sum(lsum, M, sm, lv_out + 1);
+  if (t == 0) lv_out[0] = 1.0;
+  __syncthreads();
+}
+
+// --- the order-1 float64 Gram / self levels ---------------------------------
+struct GramArgs {
+  Geo G;
+  int mode;  // 0 rect pairs (rows [row_begin, row_end)), 1 symmetric (j >= i), 2 self
+  int64_t row_begin, rows;
+  int norm;
+  const double *diag_x, *diag_y;
+  double *K;
+  int64_t ldk;
+  double *levels;
+  double *self_out;
+  double *scratch;
+  int64_t slot;  // doubles of scratch per CTA
+};
+
+__global__ void __launch_bounds__(RT) gram_kernel(GramArgs A) {
+  __shared__ double sm[NW * (VMAX + 1) + NW + 2 * (GEN_MAX_LEVELS + 1)];
+  double *lv = sm + NW * (VMAX + 1) + NW;
+  const Geo &G = A.G;
+  double *colacc = A.scratch + blockIdx.x * A.slot;
+  const int64_t npairs = A.mode == 2 ? G.nx : A.rows * G.ny;
+  for (int64_t g = blockIdx.x; g < npairs; g += gridDim.x) {
+    int64_t i, j;
+    if (A.mode == 2) {
+      i = j = g;
+    } else {
+      i = A.row_begin + g / G.ny;
+      j = g % G.ny;
+      if (A.mode == 1 && j < i) continue;  // CTA-uniform
+    }
+    const double *xs = G.X + i * G.lx * G.d;
+    const double *ys = (A.mode == 2 ? G.X : G.Y) + j * (A.mode == 2 ? G.lx : G.ly) * G.d;
+    cta_pair_levels(G, xs, G.lx, ys, A.mode == 2 ? G.lx : G.ly, colacc, sm, lv);
+    if (threadIdx.x == 0) {
+      const int M = G.M;
+      if (A.mode == 2) {
+        for (int m = 0; m <= M; ++m) A.self_out[i * (M + 1) + m] = lv[m];
+      } else {
+        const bool sym = A.mode == 1;
+        const int64_t row = sym ? i : i - A.row_begin;
+        if (A.levels) {
+          for (int m = 0; m <= M; ++m) A.levels[(row * A.ldk + j) * (M + 1) + m] = lv[m];
+          if (sym && j != i)
+            for (int m = 0; m <= M; ++m) A.levels[(j * A.ldk + i) * (M + 1) + m] = lv[m];
+        }
+        if (A.K) {
+          const double v = finish_entry(lv, M, A.norm, A.diag_x ? A.diag_x + i * (M + 1) : nullptr,
+                                        A.diag_y ? A.diag_y + j * (M + 1) : nullptr);
+          A.K[row * A.ldk + j] = v;
+          if (sym && j != i) A.K[j * A.ldk + i] = v;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// --- certification of the FP32 paths -----------------------------------------
+struct CertArgs {
+  Geo G;
+  int symmetric;
+  int64_t row_begin, rows;
+  int norm;
+  const double *diag_x, *diag_y;
+  const float *k1buf;  // FP32 level 1 per entry [row][ny], or null
+  double *K;
+  int64_t ldk;
+  double *levels;
+  double *scratch;
+  int64_t slot;
+};
+
+// Pass 1 (every thread one entry at a time): the exact-level-1 check. Entries
+// whose FP32 level 1 deviates from the telescoped value by more than the
+// tolerance of their scale are marked NaN (with the mirror); the others are
+// corrected to the exact level 1.
+__global__ void cert_scan_kernel(CertArgs A) {
+  const Geo &G = A.G;
+  const int M = G.M;
+  const bool sym = A.symmetric;
+  const int64_t total = A.rows * G.ny;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += nthr) {
+    const int64_t r = e / G.ny, j = e % G.ny;
+    const int64_t i = A.row_begin + r;
+    const int64_t row = sym ? i : r;
+    if (sym && j <= i) continue;  // the diagonal of K(X) is the self levels' own
+    double *kp = A.K + row * A.ldk + j;
+    const double v = *kp;
+    if (isnan(v)) continue;
+    const double k1e = exact_level1(G.S, G.X + i * G.lx * G.d, G.lx, G.Y + j * G.ly * G.d, G.ly,
+                                    (int)G.d);
+    const double delta = k1e - (double)A.k1buf[row * G.ny + j];
+    double scale = CERT_NOISE_RAW / CERT_NOISE * fabs(v), corr = delta;
+    if (A.norm != SK_NORM_NONE) {
+      const double *px = A.diag_x + i * (M + 1), *py = A.diag_y + j * (M + 1);
+      scale = sqrt(fabs(px[1] * py[1]));
+      if (A.norm == SK_NORM_LEVELWISE) {
+        const double den = sqrt((px[1] > 0.0 ? px[1] : 0.0) * (py[1] > 0.0 ? py[1] : 0.0));
+        corr = den > 0.0 ? delta / den / (double)(M + 1) : 0.0;
+      } else {
+        double sx = 0.0, sy = 0.0;
+        for (int m = 0; m <= M; ++m) {
+          sx += px[m];
+          sy += py[m];
+        }
+        corr = delta / sqrt(sx * sy);
+      }
+    }
+    const double nv = fabs(delta) > CERT_NOISE * scale
+                          ? __longlong_as_double(0x7ff8000000000000ll)
+                          : v + corr;
+    *kp = nv;
+    if (sym) A.K[j * A.ldk + i] = nv;
+    if (A.levels && !isnan(nv)) {
+      A.levels[(row * A.ldk + j) * (M + 1) + 1] = k1e;
+      if (sym) A.levels[(j * A.ldk + i) * (M + 1) + 1] = k1e;
+    }
+  }
+}
+
+// Pass 2: CTAs stride over the entries RT at a time and recompute every NaN
+// entry in float64, one pair (plus both self levels when normalised) per CTA.
+__global__ void __launch_bounds__(RT) cert_redo_kernel(CertArgs A) {
+  __shared__ double sm[NW * (VMAX + 1) + NW + 3 * (GEN_MAX_LEVELS + 1)];
+  __shared__ int64_t list[RT];
+  __shared__ int cnt;
+  double *lv = sm + NW * (VMAX + 1) + NW, *dx = lv + GEN_MAX_LEVELS + 1, *dy = dx + GEN_MAX_LEVELS + 1;
+  const Geo &G = A.G;
+  const int M = G.M;
+  const bool sym = A.symmetric;
+  double *colacc = A.scratch + blockIdx.x * A.slot;
+  const int64_t total = A.rows * G.ny;
+  for (int64_t e0 = (int64_t)blockIdx.x * RT; e0 < total; e0 += (int64_t)gridDim.x * RT) {
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    const int64_t e = e0 + threadIdx.x;
+    if (e < total) {
+      const int64_t r = e / G.ny, j = e % G.ny, i = A.row_begin + r;
+      const int64_t row = sym ? i : r;
+      if (!(sym && j < i) && isnan(A.K[row * A.ldk + j])) list[atomicAdd(&cnt, 1)] = e;
+    }
+    __syncthreads();
+    const int n = cnt;
+    __syncthreads();  // every thread has read cnt before it is reset
+    for (int q = 0; q < n; ++q) {
+      const int64_t ee = list[q];
+      const int64_t r = ee / G.ny, j = ee % G.ny, i = A.row_begin + r;
+      const int64_t row = sym ? i : r;
+      const double *xs = G.X + i * G.lx * G.d, *ys = G.Y + j * G.ly * G.d;
+      cta_pair_levels(G, xs, G.lx, ys, G.ly, colacc, sm, lv);
+      if (A.norm != SK_NORM_NONE) {
+        cta_pair_levels(G, xs, G.lx, xs, G.lx, colacc, sm, dx);
+        cta_pair_levels(G, ys, G.ly, ys, G.ly, colacc, sm, dy);
+      }
+      if (threadIdx.x == 0) {
+        const double v =
+            finish_entry(lv, M, A.norm, A.norm != SK_NORM_NONE ? dx : nullptr,
+                         A.norm != SK_NORM_NONE ? dy : nullptr);
+        A.K[row * A.ldk + j] = v;
+        if (sym && j != i) A.K[j * A.ldk + i] = v;
+        if (A.levels) {
+          for (int m = 0; m <= M; ++m) A.levels[(row * A.ldk + j) * (M + 1) + m] = lv[m];
+          if (sym && j != i)
+            for (int m = 0; m <= M; ++m) A.levels[(j * A.ldk + i) * (M + 1) + m] = lv[m];
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Self levels: level 1 -> exact; noisy, negative or non-finite -> float64.
+__global__ void __launch_bounds__(RT) self_cert_kernel(Geo G, double *out, double *scratch,
+                                                       int64_t slot) {
+  __shared__ double sm[NW * (VMAX + 1) + NW + (GEN_MAX_LEVELS + 1)];
+  __shared__ int redo;
+  double *lv = sm + NW * (VMAX + 1) + NW;
+  const int M = G.M;
+  double *colacc = scratch + blockIdx.x * slot;
+  for (int64_t i = blockIdx.x; i < G.nx; i += gridDim.x) {
+    double *o = out + i * (M + 1);
+    const double *x = G.X + i * G.lx * G.d;
+    if (threadIdx.x == 0) {
+      bool bad = false;
+      for (int m = 1; m <= M; ++m) bad |= !(o[m] >= 0.0) || isinf(o[m]);
+      if (!bad && G.difference && M >= 1) {
+        const double k1e = exact_level1(G.S, x, G.lx, x, G.lx, (int)G.d);
+        if (fabs(o[1] - k1e) > CERT_NOISE * fabs(k1e))
+          bad = true;
+        else
+          o[1] = k1e;
+      }
+      redo = bad;
+    }
+    __syncthreads();
+    if (redo) {
+      cta_pair_levels(G, x, G.lx, x, G.lx, colacc, sm, lv);
+      if (threadIdx.x == 0)
+        for (int m = 0; m <= M; ++m) o[m] = lv[m];
+    }
+    __syncthreads();
+  }
+}
+
+Geo geo(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny, int64_t ly,
+        int64_t d, const sk_kernel_config &c) {
+  Geo G;
+  G.X = X;
+  G.Y = Y;
+  G.nx = nx;
+  G.lx = lx;
+  G.ny = ny;
+  G.ly = ly;
+  G.d = d;
+  G.S = to_static(c.static_spec);
+  G.M = c.n_levels;
+  G.difference = c.difference;
+  return G;
+}
+
+int64_t slot_doubles(int64_t lx, int64_t ly, const sk_kernel_config &c) {
+  const int64_t L = std::max(lx, ly);
+  const int64_t T = c.difference ? std::max<int64_t>(L - 1, 1) : std::max<int64_t>(L, 1);
+  return std::max(c.n_levels - 1, 1) * T;
+}
+
+int64_t grid_for(int64_t work, int64_t slot) {
+  // enough CTAs to fill the machine, scratch within 256 MiB
+  const int64_t cap = std::max<int64_t>(1, (256ll << 20) / (slot * 8));
+  return std::max<int64_t>(1, std::min<int64_t>({work, (int64_t)sm_count() * 4, cap}));
+}
+
+}  // namespace rowscan
+
+bool rowscan_supported(int64_t lx, int64_t ly, const sk_kernel_config &c) {
+  const int64_t L = std::max(lx, ly);
+  const int64_t T = c.difference ? L - 1 : L;
+  const int p = std::max(1, std::min(c.order, std::max(c.n_levels, 1)));
+  return p == 1 && c.n_levels <= GEN_MAX_LEVELS && T <= (int64_t)rowscan::RT * rowscan::CMAX;
+}
+
+size_t rowscan_workspace_bytes(int64_t npairs, int64_t lx, int64_t ly, const sk_kernel_config &c) {
+  using namespace rowscan;
+  const int64_t slot = slot_doubles(lx, ly, c);
+  return (size_t)grid_for(std::max<int64_t>(npairs, 1), slot) * slot * 8;
+}
+
+int rowscan_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny,
+                 int64_t ly, int64_t d, int mode, const sk_kernel_config &c, int64_t row_begin,
+                 int64_t row_end, const double *diag_x, const double *diag_y, double *K,
+                 int64_t ldk, double *levels, double *self_out, void *ws, size_t ws_bytes,
+                 cudaStream_t st) {
+  using namespace rowscan;
+  GramArgs A{};
+  A.G = geo(X, nx, lx, Y, ny, ly, d, c);
+  A.mode = mode;
+  A.row_begin = row_begin;
+  A.rows = row_end - row_begin;
+  A.norm = c.normalization;
+  A.diag_x = diag_x;
+  A.diag_y = diag_y;
+  A.K = K;
+  A.ldk = ldk;
+  A.levels = levels;
+  A.self_out = self_out;
+  const int64_t npairs = mode == 2 ? nx : A.rows * ny;
+  if (npairs <= 0) return SK_OK;
+  A.slot = slot_doubles(lx, mode == 2 ? lx : ly, c);
+  const int64_t grid = grid_for(npairs, A.slot);
+  if (!ws || ws_bytes < (size_t)(grid * A.slot * 8))
+    return fail(SK_ERR_WORKSPACE, "workspace too small for the float64 row-scan kernel");
+  A.scratch = (double *)ws;
+  gram_kernel<<<(unsigned)grid, RT, 0, st>>>(A);
+  SK_CHECK_LAUNCH();
+  return SK_OK;
+}
+
+size_t cert_workspace_bytes(int64_t lx, int64_t ly, const sk_kernel_config &c) {
+  using namespace rowscan;
+  const int64_t slot = slot_doubles(lx, ly, c);
+  return (size_t)grid_for(1ll << 40, slot) * slot * 8;
+}
+
+int cert_fixup(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny, int64_t ly,
+               int64_t d, int symmetric, const sk_kernel_config &c, int64_t row_begin,
+               int64_t row_end, const double *diag_x, const double *diag_y, const float *k1buf,
+               double *K, int64_t ldk, double *levels, void *ws, size_t ws_bytes,
+               cudaStream_t st) {
+  using namespace rowscan;
+  CertArgs A{};
+  A.G = geo(X, nx, lx, Y, ny, ly, d, c);
+  A.symmetric = symmetric;
+  A.row_begin = row_begin;
+  A.rows = row_end - row_begin;
+  A.norm = c.normalization;
+  A.diag_x = diag_x;
+  A.diag_y = diag_y;
+  A.k1buf = k1buf;
+  A.K = K;
+  A.ldk = ldk;
+  A.levels = levels;
+  const int64_t total = A.rows * ny;
+  if (total <= 0) return SK_OK;
+  if (k1buf && c.difference && c.n_levels >= 1) {
+    const unsigned g = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 8);
+    cert_scan_kernel<<<g, 256, 0, st>>>(A);
+    SK_CHECK_LAUNCH();
+  }
+  A.slot = slot_doubles(lx, ly, c);
+  const int64_t grid = std::min<int64_t>(grid_for(1ll << 40, A.slot), (total + RT - 1) / RT);
+  if (!ws || ws_bytes < (size_t)(grid * A.slot * 8))
+    return fail(SK_ERR_WORKSPACE, "workspace too small for the certification fix-up");
+  A.scratch = (double *)ws;
+  cert_redo_kernel<<<(unsigned)grid, RT, 0, st>>>(A);
+  SK_CHECK_LAUNCH();
+  return SK_OK;
+}
+
+int cert_self_fixup(const double *X, int64_t n, int64_t l, int64_t d, const sk_kernel_config &c,
+                    double *out, void *ws, size_t ws_bytes, cudaStream_t st) {
+  using namespace rowscan;
+  if (n <= 0) return SK_OK;
+  const Geo G = geo(X, n, l, X, n, l, d, c);
+  const int64_t slot = slot_doubles(l, l, c);
+  const int64_t grid = grid_for(n, slot);
+  if (!ws || ws_bytes < (size_t)(grid * slot * 8))
+    return fail(SK_ERR_WORKSPACE, "workspace too small for the self-level fix-up");
+  self_cert_kernel<<<(unsigned)grid, RT, 0, st>>>(G, out, (double *)ws, slot);
+  SK_CHECK_LAUNCH();
+  return SK_OK;
+}
+
+}  // namespace sk

@@ -119,7 +119,7 @@ def self_levels(X, cfg: KernelConfig, precision: str = "fp32", device=None) -> t
 
 
 def _self_levels_t(Xt: torch.Tensor, cfg: KernelConfig, precision: str,
-                   c=None, ws=None) -> torch.Tensor:
+                   c=None, ws=None, flags: int = 0) -> torch.Tensor:
     lib = _native.load()
     dev = Xt.device
     n, L, d = Xt.shape
@@ -127,7 +127,7 @@ def _self_levels_t(Xt: torch.Tensor, cfg: KernelConfig, precision: str,
     out = torch.empty((n, M + 1), dtype=torch.float64, device=dev)
     if n == 0:
         return out
-    c = c or _native.config_struct(cfg, precision)
+    c = c or _native.config_struct(cfg, precision, flags)
     with torch.cuda.device(dev):  # workspace sizes depend on the device's SM count
         if ws is None:
             ws = _workspace(lib.sk_workspace_bytes(n, L, 0, 0, d, c), dev)
@@ -141,12 +141,14 @@ def _self_levels_t(Xt: torch.Tensor, cfg: KernelConfig, precision: str,
 def gram_block(Xt: torch.Tensor, Yt: torch.Tensor | None, cfg: KernelConfig,
                row_begin: int = 0, row_end: int | None = None, precision: str = "fp32",
                diag_x=None, diag_y=None, K=None, want_levels: bool = False,
-               check_global: bool = True):
+               check_global: bool = True, flags: int = 0):
     """Rows [row_begin, row_end) of the Gram on device tensors (the sk_gram call).
 
     Yt=None is the symmetric K(X): K must then be the full (N, N) matrix (it is
     allocated if omitted) and only pairs i <= j with i in the row range are
-    evaluated and mirrored. Returns (K, levels-or-None).
+    evaluated and mirrored. Returns (K, levels-or-None). `flags`:
+    `_native.SK_FLAG_NO_FIXUP` leaves the FP32 certification's NaN markers in
+    K (diagnostics; see include/sigkern_b200.h).
     """
     lib = _native.load()
     dev = Xt.device
@@ -155,7 +157,7 @@ def gram_block(Xt: torch.Tensor, Yt: torch.Tensor | None, cfg: KernelConfig,
     ny, ly = (nx, lx) if sym else Yt.shape[:2]
     row_end = nx if row_end is None else row_end
     M = cfg.n_levels
-    c = _native.config_struct(cfg, precision)
+    c = _native.config_struct(cfg, precision, flags)
     with torch.cuda.device(dev):  # workspace sizes depend on the device's SM count
         ws = _workspace(lib.sk_workspace_bytes(nx, lx, ny, ly, d, c), dev)
     if cfg.normalization != "none":

@@ -25,7 +25,7 @@ def test_library_loads_and_exports_header_symbols():
     assert set(names) == set(_native.EXPORTS)
     for n in names:
         assert hasattr(lib, n), n
-    assert lib.sk_abi_version() == 1
+    assert lib.sk_abi_version() == 2
     assert lib.sk_last_error() == b""
 
 
@@ -68,14 +68,26 @@ def test_fast_path_selection():
     assert lib.sk_fast_path(2, 256, 4, c3) == 0             # x shorter than the wavefront
 
 
+def lib_fixup_bytes(L, M, p=1):
+    # sk_generic.cu fixup_workspace_bytes: one float64 scratch slot per thread
+    # (column state (M-1)*(L-1)*p + L + 1 doubles), threads = min(148*2*128,
+    # 96 MiB / slot) rounded down to 128
+    slot = ((M - 1) * (L - 1) * p + L + 1) * 8
+    thr = min(148 * 2 * 128, (96 << 20) // slot) // 128 * 128
+    return max(thr, 128) * slot
+
+
 def test_workspace_sizes():
     lib = _native.load()
     c3 = _native.config_struct(KernelConfig(n_levels=5, normalization="levelwise"))
     n, L, d = 8192, 256, 16
     ws = lib.sk_workspace_bytes(n, L, n, L, d, c3)
-    # packed fp32 x role (row pairs, 2*16+4 floats) + y role (16+4 floats per point)
-    # + the midrange codes of the centring (2d u64, 256-byte aligned)
-    assert ws == n * (L // 2) * 36 * 4 + n * L * 20 * 4 + 256
+    # the certification's FP32 level-1 buffer (n x n floats), then the larger of
+    # the packed roles (x row pairs of 2*16+4 floats, y points of 16+4 floats, the
+    # midrange codes of the centring: 2d u64, 256-byte aligned) and the fix-up scratch
+    roles = n * (L // 2) * 36 * 4 + n * L * 20 * 4 + 256
+    assert ws == n * n * 4 + max(roles, lib_fixup_bytes(L, 5))
+    assert lib.sk_abi_version() == 2
     f64 = _native.config_struct(KernelConfig(n_levels=3, order=2), "fp64")
     assert lib.sk_workspace_bytes(4, 6, 5, 7, 2, f64) > 0
 

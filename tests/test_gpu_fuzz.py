@@ -2,19 +2,20 @@
 public `sig_kernel_gram`, whatever path each one dispatches to (fused FP32,
 GEMM-fed FP32, float64), against the float64 CPU oracle.
 
-Tolerances are the north star's, 1e-5 normalised and 1e-4 unnormalised, for
-anything that touched an FP32 kernel (the Gram or either self-level pass: each
-call dispatches on its own shapes), and 1e-9 when all of them ran in float64
-(Matern kinds: 1e-7, sqrt of the norm-expansion distance near x = y).
-Relative to what: unnormalised entries against max(|R_ij|, 1e-3 max|R|);
-normalised entries, bounded by the unit diagonal, against max(|R_ij|, 1e-2).
-Normalised entries are cancelling sums of level ratios, and the seeded sweep
-found entries of 2.5e-3 (levelwise, M = 8) and 6.6e-4 (global, M = 7, self
-kernels ~3e3) whose FP32 error is 2e-7 and 1.5e-8 absolute — 9e-5 and 2e-5
-of the entry, 2e-5 and 1.5e-6 of the 1e-2 floor. Known FP32 limit (DESIGN.md
-§4): with n_levels >= 7 and short, strongly cancelling sequences the top
-levels' FP32 partial sums lose ~1e-5 relative, so normalised entries there are
-held to 5e-5 of the unit scale (seed 28: levelwise, M = 8, L ~ 60 -> 2.2e-5).
+Tolerances are the north star's, elementwise PLAIN relative error: 1e-5
+normalised and 1e-4 unnormalised for anything that touched an FP32 kernel (the
+Gram or either self-level pass), 1e-9 when everything ran in float64 (Matern
+kinds: 1e-7, sqrt of the norm-expansion distance near x = y). Only entries
+below 1e-12 of the matrix's largest are judged absolutely, and an entry
+so ill-conditioned that float64 itself cannot pin it (the reference's own
+rounding, estimated as 1e-14 x the level values of |A| — the DP on the
+absolute increments — exceeds 1e-1 x the tolerance: one-dimensional paths with
+many levels cancel terms ~1e12 times larger than the result) is held to that
+float64 bound instead. The FP32 paths meet
+this through their certification: entries the FP32 arithmetic cannot vouch for
+(cancelling level sums, noisy increments) are recomputed in float64 inside
+sk_gram (include/sigkern_b200.h). Seeds 96-199 alternate in n_levels 7-8 on
+short sequences, where the cancellation lives.
 """
 
 import numpy as np
@@ -40,6 +41,9 @@ def _case(seed):
     lx = int(r.integers(2, 70))
     ly = int(r.integers(2, 70)) if r.random() < 0.6 else lx
     sym = bool(r.random() < 0.3)
+    if seed >= 96 and seed % 2 == 0:  # second half: many levels on short sequences
+        M = int(r.integers(7, 9))
+        lx, ly = int(r.integers(8, 40)), int(r.integers(8, 40))
     kw = {}
     if kind in ("rbf", "matern12", "matern32", "matern52", "rational_quadratic"):
         kw["bandwidth"] = float(r.uniform(0.5, 2.0))
@@ -53,7 +57,7 @@ def _case(seed):
     return kind, kw, M, order, norm, diff, d, lx, ly, sym
 
 
-@pytest.mark.parametrize("seed", range(96))
+@pytest.mark.parametrize("seed", range(200))
 def test_random_config_matches_oracle(seed):
     kind, kw, M, order, norm, diff, d, lx, ly, sym = _case(seed)
     X = gen_brownian(5, lx, d, SeedStream(seed, ("x",))).data
@@ -74,10 +78,32 @@ def test_random_config_matches_oracle(seed):
     assert K.shape == R.shape
     if sym:
         assert np.array_equal(K, K.T)
-    floor = 1e-3 * np.abs(R).max() if norm == "none" else 1e-2
-    err = float((np.abs(K - R) / np.maximum(np.abs(R), floor)).max())
     if paths == {"fp64"}:
         tol = 1e-7 if kind.startswith("matern") else 1e-9
     else:
-        tol = 1e-4 if norm == "none" else (5e-5 if M >= 7 else 1e-5)
+        tol = 1e-4 if norm == "none" else 1e-5
+    floor = np.maximum(1e-12 * np.abs(R).max(), 10 / tol * _f64_error(X, Y, kind, kw, M, order,
+                                                                        diff, norm))
+    err = float((np.abs(K - R) / np.maximum(np.abs(R), floor)).max()) if R.size else 0.0
     assert err <= tol, (paths, kind, kw, M, order, norm, diff, d, lx, ly, sym, err)
+
+
+def _f64_error(X, Y, kind, kw, M, order, diff, norm):
+    """Rounding scale of the reference's own float64 value of every entry: 1e-14 x
+    the level values of the DP on |A| (each level a sum of |terms|), normalised
+    like the entry (levelwise: by the self levels; global: by the self kernels)."""
+    sp = O.static_params(kind, **kw)
+    Yr = X if Y is None else Y
+    p = max(1, min(order, M)) if M >= 1 else 1
+    A = np.abs(O.increments(sp, X[:, None], Yr[None, :], diff))
+    mag = O.levels_dp(A, M, p)[..., 1:]
+    if norm == "none":
+        return 1e-14 * mag.sum(-1)
+    dx = O.self_levels(sp, X, M, p, diff)
+    dy = O.self_levels(sp, Yr, M, p, diff)
+    if norm == "levelwise":
+        den = np.sqrt(np.abs(dx[:, None, 1:] * dy[None, :, 1:]))
+        t = np.divide(mag, den, out=np.zeros_like(mag), where=den > 0)
+        return 1e-14 * t.sum(-1) / (M + 1)
+    sx, sy = np.abs(dx.sum(-1)), np.abs(dy.sum(-1))
+    return 1e-14 * mag.sum(-1) / np.sqrt(np.maximum(np.outer(sx, sy), 1e-300))

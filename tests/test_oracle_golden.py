@@ -139,3 +139,17 @@ def test_rfsf_fit_rff_reproduces_reference(rfsf_cases):
         for a, s in enumerate(st.slot_states):
             assert np.array_equal(s.weights, c.slots[a]["weights"]), (c.name, a)
             assert s.out_dim == 2 * c.D
+
+
+def test_c3_far_block_matches_reference():
+    """The far-end c3 golden block (rows/cols 8168-8191 of the full inputs): the
+    window of the prefix-stable generator reproduces the reference's slice, and the
+    oracle reproduces its 24 x 24 Gram (levelwise and unnormalised)."""
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "c3_far.npz"))
+    X = O.gen_brownian(24, 256, 16, 1, start=8168)
+    Y = O.gen_brownian(24, 256, 16, 2, start=8168)
+    assert np.array_equal(X, z["X"]) and np.array_equal(Y, z["Y"])
+    for norm in ("levelwise", "none"):
+        K = O.gram(X[:6], Y[:5], M=5, p=1, normalization=norm, n_threads=O.host_threads())
+        assert np.allclose(K, z[f"K_{norm}"][:6, :5], rtol=1e-12, atol=0), norm
