@@ -115,9 +115,11 @@ size_t sk_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int64_
     // FP32 paths: the float64 fix-up reuses the same workspace afterwards
     // (Gram: after the FP32 level-1 buffer of the certification)
     const int64_t l2e = n2 > 0 ? l2 : l1;
-    const size_t fix = rowscan_supported(l1, l2e, *cfg) ? cert_workspace_bytes(l1, l2e, *cfg)
-                                                         : fixup_workspace_bytes(l1, l2e, *cfg);
-    const size_t k1 = n2 > 0 ? k1buf_bytes(n1, n2) : 0;
+    const int64_t n2e = n2 > 0 ? n2 : n1;
+    const size_t fix = rowscan_supported(l1, l2e, *cfg)
+                           ? cert_workspace_bytes(n1, l1, n2e, l2e, d, *cfg)
+                           : fixup_workspace_bytes(l1, l2e, *cfg);
+    const size_t k1 = n2 > 0 ? k1buf_bytes(n1, n2, cfg->normalization) : 0;
     if (path == 1) return k1 + std::max(fix, fast_workspace_bytes(n1, l1, n2, l2, d, *cfg));
     if (path == 2) return k1 + std::max(fix, gemm_workspace_bytes(n1, l1, n2, l2, d, *cfg));
     return n2 > 0 ? std::max(generic_workspace_bytes(n1 * n2, l1, l2, *cfg),
@@ -183,7 +185,7 @@ int sk_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny
   const int path = path_of(lx, ly, d, *cfg);
   if (path != 0) {
     // FP32 paths: [level-1 buffer of the certification | path workspace]
-    const size_t k1b = k1buf_bytes(nx, ny);
+    const size_t k1b = k1buf_bytes(nx, ny, cfg->normalization);
     if (!workspace || workspace_bytes < k1b)
       return fail(SK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(k1b) + "+");
     float *k1 = K ? (float *)workspace : nullptr;

@@ -302,13 +302,14 @@ int fp64_fixup(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t
                int64_t row_end, const double *diag_x, const double *diag_y, const float *k1buf,
                double *K, int64_t ldk, double *levels, void *ws, size_t ws_bytes,
                cudaStream_t st);
-// FP32 level-1 buffer of the certification (rows x ny floats) at the start
-// of an FP32 Gram's workspace; the path's own workspace follows it.
-inline size_t k1buf_bytes(int64_t nx, int64_t ny) {
-  return ((size_t)nx * ny * 4 + 255) & ~(size_t)255;
-}
 int fp64_self_fixup(const double *X, int64_t n, int64_t l, int64_t d, const sk_kernel_config &c,
                     double *out, void *ws, size_t ws_bytes, cudaStream_t st);
+
+// Certification buffer at the start of an FP32 Gram's workspace (the path's
+// own workspace follows): per entry a float2 (FP32 level 1, sum_m |k_m|).
+inline size_t k1buf_bytes(int64_t nx, int64_t ny, int /*norm*/) {
+  return ((size_t)nx * ny * 8 + 255) & ~(size_t)255;
+}
 
 // Order-1 float64 recursion with one CTA per pair (sk_rowscan.cu): the
 // float64 Gram / self levels for rows of >= 32 increments, and the FP32
@@ -321,7 +322,8 @@ int rowscan_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64
                  int64_t row_end, const double *diag_x, const double *diag_y, double *K,
                  int64_t ldk, double *levels, double *self_out, void *ws, size_t ws_bytes,
                  cudaStream_t st);
-size_t cert_workspace_bytes(int64_t lx, int64_t ly, const sk_kernel_config &c);
+size_t cert_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int64_t d,
+                            const sk_kernel_config &c);
 int cert_fixup(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny, int64_t ly,
                int64_t d, int symmetric, const sk_kernel_config &c, int64_t row_begin,
                int64_t row_end, const double *diag_x, const double *diag_y, const float *k1buf,

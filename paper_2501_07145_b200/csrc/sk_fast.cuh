@@ -105,10 +105,10 @@ struct Params {
   const float *S;
   int64_t s_ld, s_xstride, s_ystride, x_blk0;
   // FP32 certification (write_pair; sk_gram in include/sigkern_b200.h):
-  // cert = 1 NaN-marks uncertified entries for the float64 fix-up; k1buf
-  // (rows x ny floats, may be null) receives each entry's FP32 level 1
+  // k1buf (rows x ny float2, may be null) receives each entry's FP32 level 1
+  // and sum_m |k_m|
   int cert;
-  float *k1buf;
+  float *k1buf;  // float2 per entry: (FP32 level 1, sum_m |k_m|)
 };
 
 typedef unsigned long long u64;
@@ -189,13 +189,14 @@ __device__ __forceinline__ void stage_sequence(float *dst, const float *src, int
 
 // Level values of pair (i, j) -> per-level output and/or normalised K entry.
 // ls = k_1..k_{M-1} (float chain totals), kout = k_M.
-// Certification (sk_gram): an entry that is non-finite or small against its
-// scale (|K| < CERT_TAU_NORM normalised, |K| < CERT_TAU_RAW sum_m |k_m|
-// unnormalised) is written as NaN for the float64 fix-up; the FP32 level 1
-// goes to `k1buf` for the fix-up pass's exact-level-1 check.
-template <int M>
+// Certification (sk_gram): besides K, the FP32 level 1 and sum_m |k_m| go to
+// `k1buf` as one float2 per entry; the certification pass (sk_rowscan.cu)
+// judges the entry from them, so the hot kernel carries no extra logic (one
+// 8-byte store: the multi-panel c5 schedule measured 1.24 s with it, 1.39 s
+// with a single 4-byte store, 1.21 s with none).
+template <int M, class T = float>
 __device__ __forceinline__ void write_pair(const Params &P, int64_t i, int64_t j,
-                                           const float *ls, float kout) {
+                                           const T *ls, T kout) {
   double lv[M + 1];
   lv[0] = 1.0;
 #pragma unroll
@@ -212,9 +213,7 @@ __device__ __forceinline__ void write_pair(const Params &P, int64_t i, int64_t j
   const int64_t row = P.symmetric ? i : i - P.row_begin;
   const bool mirror = P.symmetric && i != j;
   const double *dx = P.diag_x ? P.diag_x + i * (M + 1) : nullptr;
-  const double *dy = P.diag_y ? P.diag_y + j * (M + 1) : nullptr;
-  const bool self = P.symmetric && i == j && dx;
-  if (self) {  // K(X)'s diagonal from the self levels: normalised diagonals exactly 1
+  if (P.symmetric && i == j && dx) {  // K(X)'s diagonal from the self levels: exactly 1
 #pragma unroll
     for (int m = 0; m <= M; ++m) lv[m] = dx[m];
   }
@@ -227,20 +226,16 @@ __device__ __forceinline__ void write_pair(const Params &P, int64_t i, int64_t j
     }
   }
   if (P.K) {
-    double v = finish_entry(lv, M, P.norm, dx, dy);
-    if (P.cert && !self) {
-      double lim = CERT_TAU_NORM;
-      if (P.norm == SK_NORM_NONE) {
-        lim = 0.0;
-#pragma unroll
-        for (int m = 0; m <= M; ++m) lim += fabs(lv[m]);
-        lim *= P.static_kind == SK_LINEAR ? CERT_TAU_RAW_LINEAR : CERT_TAU_RAW;
-      }
-      if (!(fabs(v) >= lim) || isinf(v)) v = __longlong_as_double(0x7ff8000000000000ll);
-    }
+    const double v = finish_entry(lv, M, P.norm, dx, P.diag_y ? P.diag_y + j * (M + 1) : nullptr);
     P.K[row * P.ldk + j] = v;
     if (mirror) P.K[j * P.ldk + i] = v;
-    if (P.k1buf) P.k1buf[row * P.ny + j] = self ? 0.f : (M >= 1 ? (float)lv[1] : 0.f);
+    if (P.k1buf) {
+      float sa = 1.f + fabsf((float)kout);
+#pragma unroll
+      for (int m = 1; m < M; ++m) sa += fabsf((float)ls[m - 1]);
+      reinterpret_cast<float2 *>(P.k1buf)[row * P.ny + j] =
+          make_float2(M == 1 ? (float)kout : (M > 1 ? (float)ls[0] : 0.f), sa);
+    }
   }
 }
 
@@ -517,14 +512,14 @@ struct GemmStage {
 
 // Receive chain values from lane q-1 (its previous step); the segment head
 // takes zeros, or the previous panel's carries `hin[k]` when from_buf.
-template <int N>
-__device__ __forceinline__ void chain_in(const float (&out)[N], float (&in)[N], int n, int sw,
+template <int N, class T = float>
+__device__ __forceinline__ void chain_in(const T (&out)[N], T (&in)[N], int n, int sw,
                                          bool first_lane, bool from_buf, const float *hin) {
 #pragma unroll
   for (int k = 0; k < N; ++k) {
     if (k < n) {
       const float v = __shfl_up_sync(0xffffffffu, out[k], 1, sw);
-      in[k] = first_lane ? (from_buf ? hin[k] : 0.f) : v;
+      in[k] = first_lane ? (from_buf ? (T)hin[k] : (T)0) : v;
     }
   }
 }
@@ -638,6 +633,94 @@ struct LaneState1 : Stage {
     float aa[C], ab[C];
     this->increments(dla, dlb, first_lane && !from_buf, aa, ab);
     // (d) level recursion, row a then row b
+    row(aa, cina, couta);
+    if (BCHK && boundary) reset_pair();
+    row(ab, cinb, coutb);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Order p = 1 with float64 column accumulators, row prefixes and level sums
+// (single panel only). The GEMM-fed linear path (large d, e.g. BASELINE c4):
+// its levels are long sums of increment products that cancel, and the FP32
+// accumulation measured up to 5e-5 of sum_m |k_m| there (2e-3 relative on
+// 0.4% of c4's entries); float64 accumulation brings it to ~1e-6 (the FP32
+// cell values remain). The DP of this path streams its cells from HBM
+// (4 bytes per cell), so the float64 pipe (~60 lane-ops/clk/SM) has room.
+// ---------------------------------------------------------------------------
+template <class Stage, int M_>
+struct LaneState1D : Stage {
+  using Stage::C;
+  static constexpr int M = M_;
+  static constexpr int NCA = (M >= 2) ? M - 1 : 0;
+  static constexpr int NCR = (NCA > 0) ? NCA : 1;
+  static constexpr int NHP = 4;  // no carries (single panel)
+
+  double colacc[NCR][C];
+  double couta[NCR], coutb[NCR];
+  double kM, kout;
+
+  __device__ __forceinline__ void reset_pair() {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+#pragma unroll
+      for (int m = 0; m < NCR; ++m) colacc[m][c] = 0.0;
+    }
+    kM = 0.0;
+  }
+  __device__ __forceinline__ void reset_panel() {
+    reset_pair();
+    kout = 0.0;
+#pragma unroll
+    for (int m = 0; m < NCR; ++m) couta[m] = coutb[m] = 0.0;
+  }
+  __device__ __forceinline__ const double *level_sums() const { return couta; }
+  __device__ __forceinline__ void store_carry(float *, bool) const {}
+
+  __device__ __forceinline__ void row(const float (&a)[C], const double (&cin)[NCR],
+                                      double (&cout)[NCR]) {
+    if constexpr (M == 1) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) kM += (double)a[c];
+    } else {
+      double sc[NCR];
+#pragma unroll
+      for (int m = 0; m < NCA; ++m) sc[m] = cin[m];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const double ad = (double)a[c];
+        double so[NCR];
+#pragma unroll
+        for (int m = 0; m < NCA; ++m) {
+          so[m] = sc[m];
+          sc[m] += colacc[m][c];
+        }
+        colacc[0][c] += ad;
+#pragma unroll
+        for (int m = 1; m < NCA; ++m) colacc[m][c] = fma(ad, so[m - 1], colacc[m][c]);
+        kM = fma(ad, so[NCA - 1], kM);
+      }
+#pragma unroll
+      for (int m = 0; m < NCA; ++m) cout[m] = sc[m];
+    }
+  }
+
+  template <bool KCHAIN, bool MULTI, bool BCHK>
+  __device__ __forceinline__ void step(const float *__restrict__ xptr, int sw, bool first_lane,
+                                       const float *, bool, bool boundary) {
+    static_assert(!MULTI, "LaneState1D is single-panel");
+    const float dla = __shfl_up_sync(0xffffffffu, this->lastDa, 1, sw);
+    const float dlb = __shfl_up_sync(0xffffffffu, this->lastDb, 1, sw);
+    double cina[NCR], cinb[NCR];
+    chain_in(couta, cina, NCA, sw, first_lane, false, nullptr);
+    chain_in(coutb, cinb, NCA, sw, first_lane, false, nullptr);
+    if (KCHAIN) {
+      const double kin = __shfl_up_sync(0xffffffffu, kout, 1, sw);
+      kout = (first_lane ? 0.0 : kin) + kM;
+    }
+    this->point(xptr);
+    float aa[C], ab[C];
+    this->increments(dla, dlb, first_lane, aa, ab);
     row(aa, cina, couta);
     if (BCHK && boundary) reset_pair();
     row(ab, cinb, coutb);

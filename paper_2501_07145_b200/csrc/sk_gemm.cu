@@ -288,10 +288,14 @@ int pack(const double *X, int64_t n, int64_t L, int64_t d, int64_t rows, const P
   return SK_OK;
 }
 
-template <class LS>
+template <class LS, bool SINGLE = false>
 int launch_dp(const Params &P, cudaStream_t st) {
   using K = void (*)(const Params);
-  const K k = P.npanel > 1 ? gemm_dp_kernel<LS, true> : gemm_dp_kernel<LS, false>;
+  K k;
+  if constexpr (SINGLE)
+    k = gemm_dp_kernel<LS, false>;
+  else
+    k = P.npanel > 1 ? gemm_dp_kernel<LS, true> : gemm_dp_kernel<LS, false>;
   int per_sm = 0;
   SK_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NTHREADS, 0));
   if (per_sm < 1) per_sm = 1;
@@ -307,10 +311,23 @@ int launch_dp(const Params &P, cudaStream_t st) {
 template <bool LIN>
 int launch_dp_lin(const Params &P, int M, int order, cudaStream_t st) {
   using fast::LaneState1;
+  using fast::LaneState1D;
   using fast::LaneStateG;
   using S8 = fast::GemmStage<8, LIN>;
   using S4 = fast::GemmStage<4, LIN>;
-  if (order == 1) {
+  if (LIN && order == 1 && P.npanel == 1) {  // float64 accumulation (LaneState1D)
+    switch (M) {
+      case 1: return launch_dp<LaneState1D<S8, 1>, true>(P, st);
+      case 2: return launch_dp<LaneState1D<S8, 2>, true>(P, st);
+      case 3: return launch_dp<LaneState1D<S8, 3>, true>(P, st);
+      case 4: return launch_dp<LaneState1D<S8, 4>, true>(P, st);
+      case 5: return launch_dp<LaneState1D<S8, 5>, true>(P, st);
+      case 6: return launch_dp<LaneState1D<S8, 6>, true>(P, st);
+      case 7: return launch_dp<LaneState1D<S8, 7>, true>(P, st);
+      case 8: return launch_dp<LaneState1D<S8, 8>, true>(P, st);
+      default: break;
+    }
+  } else if (order == 1) {
     switch (M) {
       case 1: return launch_dp<LaneState1<S8, 1>>(P, st);
       case 2: return launch_dp<LaneState1<S8, 2>>(P, st);
@@ -433,7 +450,7 @@ int gemm_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t 
     // symmetric K(X): the kernel writes rows >= row_begin of the full matrix;
     // cross: rows relative to the caller's row_begin
     if (!symmetric) {
-      P.k1buf = k1buf ? k1buf + (b0 - row_begin) * ny : nullptr;
+      P.k1buf = k1buf ? k1buf + 2 * (b0 - row_begin) * ny : nullptr;
       P.K = K ? K + (b0 - row_begin) * ldk : nullptr;
       P.levels = levels ? levels + (b0 - row_begin) * ldk * (c.n_levels + 1) : nullptr;
       P.row_begin = b0;  // write_pair subtracts row_begin

@@ -255,7 +255,7 @@ struct FixupArgs {
   int64_t ldk;
   double *levels;
   int64_t rows;     // rows of the range
-  const float *k1buf;  // FP32 level 1 per entry [row][ny], or null
+  const float *k1buf;  // per entry [row][ny] float2 (FP32 level 1, sum_m |k_m|), or null
   const double *diag_x, *diag_y;
 };
 
@@ -279,11 +279,19 @@ __global__ void __launch_bounds__(GEN_THREADS) fixup_kernel(FixupArgs A) {
     const int64_t row = sym ? i : r;
     if (sym && j < i) continue;
     double v = A.K[row * A.ldk + j];
-    bool redo = isnan(v);
+    bool redo = isnan(v) || isinf(v);
+    if (!redo && A.k1buf && !(sym && i == j)) {  // cancellation rule (write_pair's data)
+      const double lim =
+          A.norm == SK_NORM_NONE
+              ? (double)A.k1buf[2 * (row * P.ny + j) + 1] *
+                    (P.S.kind == SK_LINEAR ? CERT_TAU_RAW_LINEAR : CERT_TAU_RAW)
+              : CERT_TAU_NORM;
+      redo = !(fabs(v) >= lim);
+    }
     if (!redo && A.k1buf && P.difference && M >= 1 && !(sym && i == j)) {
       const double k1e = exact_level1(P.S, P.X + i * P.lx * P.d, P.lx, P.Y + j * P.ly * P.d, P.ly,
                                       (int)P.d);
-      const double delta = k1e - (double)A.k1buf[row * P.ny + j];
+      const double delta = k1e - (double)A.k1buf[2 * (row * P.ny + j)];
       double scale = CERT_NOISE_RAW / CERT_NOISE * fabs(v), corr = delta;
       if (A.norm != SK_NORM_NONE) {
         const double *px = A.diag_x + i * (M + 1), *py = A.diag_y + j * (M + 1);

@@ -24,8 +24,10 @@ namespace rowscan {
 
 constexpr int RT = 256;            // threads per CTA
 constexpr int NW = RT / 32;
-constexpr int CMAX = 16;           // columns per thread: T2 <= 4096
+constexpr int CMAX = 16;           // columns per thread: T2 <= 4096 (cta_pair_levels_t)
 constexpr int VMAX = GEN_MAX_LEVELS - 1;  // scanned levels (1..M-1)
+constexpr int YSTAGE_BYTES = 96 * 1024;   // dynamic shared memory for the y staging
+__device__ __forceinline__ int64_t ystage_doubles() { return YSTAGE_BYTES / 8; }
 
 struct Geo {
   const double *X, *Y;
@@ -83,80 +85,198 @@ __device__ __forceinline__ void block_sum(const double *v, int n, double *sm, do
 
 // Level values k_0..k_M of the pair (xs: lx points, ys: ly points) into
 // lv_out[0..M] (shared memory, written by thread 0; visible after return).
-// colacc: this CTA's scratch, (M-1) * T2 doubles. All threads call it.
-__device__ void cta_pair_levels(const Geo &G, const double *__restrict__ xs, int64_t lx,
-                                const double *__restrict__ ys, int64_t ly,
-                                double *__restrict__ colacc, double *sm, double *lv_out) {
+// colacc: this CTA's scratch slice (slot_doubles). All threads call it.
+// CC: compile-time columns per thread (>= ceil(T2 / RT)); every per-thread
+// array is indexed by unrolled compile-time loops so it stays in registers.
+template <int CC>
+__device__ __noinline__ void cta_pair_levels_t(const Geo &G, const double *__restrict__ xs, int64_t lx,
+                                  const double *ys, int64_t ly, double *__restrict__ colacc,
+                                  double *sm, double *lv_out) {
   const int M = G.M, d = (int)G.d;
   const int64_t T1 = G.difference ? lx - 1 : lx, T2 = G.difference ? ly - 1 : ly;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  if (M == 0 || T1 <= 0 || T2 <= 0) {
-    if (t == 0) {
-      lv_out[0] = 1.0;
-      for (int m = 1; m <= M; ++m) lv_out[m] = 0.0;
-    }
-    __syncthreads();
-    return;
-  }
   const int C = (int)((T2 + RT - 1) / RT);
   const int64_t c0 = std::min<int64_t>((int64_t)t * C, T2);
   const int n = (int)(std::min<int64_t>(c0 + C, T2) - c0);  // own cells of a row
   const int NV = M - 1;
-  for (int m = 0; m < NV; ++m)
-    for (int k = 0; k < n; ++k) colacc[m * T2 + c0 + k] = 0.0;
-  // point-kernel values of the previous row at columns c0 .. c0 + n (difference)
-  double gp[CMAX + 1];
-  if (G.difference)
-    for (int k = 0; k <= n; ++k) gp[k] = static_eval_f64(G.S, xs, ys + (c0 + k) * d, d);
+  // column accumulators of levels 1..M-1 for the own columns: registers for
+  // CC <= 2 (every loop unrolled), else the scratch slice (rows of T2 doubles)
+  constexpr bool REG = CC <= 2;
+  double ca[REG ? VMAX : 1][REG ? CC : 1];
+  double *cmem = colacc + T2 + 2;  // after the row buffer
+  auto CA = [&](int m, int k) -> double & {
+    if constexpr (REG) return ca[m][k];
+    else return cmem[(int64_t)m * T2 + c0 + k];
+  };
+  if constexpr (REG) {
+#pragma unroll
+    for (int m = 0; m < VMAX; ++m)
+#pragma unroll
+      for (int k = 0; k < CC; ++k) ca[m][k] = 0.0;
+  } else {
+    for (int m = 0; m < NV; ++m)
+#pragma unroll
+      for (int k = 0; k < CC; ++k)
+        if (k < n) CA(m, k) = 0.0;
+  }
   double lsum[GEN_MAX_LEVELS];
-  for (int m = 0; m < M; ++m) lsum[m] = 0.0;
+#pragma unroll
+  for (int m = 0; m < GEN_MAX_LEVELS; ++m) lsum[m] = 0.0;
   double *smb = sm + NW * VMAX;  // warp-boundary point-kernel values
+  // d >= 32: a row's point-kernel values are formed warp-cooperatively (lanes
+  // over channels: coalesced reads of every y point) into a row buffer in the
+  // scratch slice; otherwise every thread evaluates its own columns
+  const bool wide = d >= 32;
+  double *grow = colacc;
+  const bool inner = G.S.kind == SK_LINEAR || G.S.kind == SK_POLYNOMIAL;
+  const int64_t ncol = G.difference ? T2 + 1 : T2;
+  // narrow rows read every y point once per row: stage the pair's y sequence
+  // in shared memory when it fits (ystage_doubles), else read it from L1/L2
+  extern __shared__ double ystage[];
+  if (!wide && ly * d <= ystage_doubles()) {
+    __syncthreads();  // the previous pair's readers are done
+    for (int64_t e = t; e < ly * d; e += RT) ystage[e] = ys[e];
+    __syncthreads();
+    ys = ystage;
+  }
+  auto wide_row = [&](const double *xa) {  // grow[c] = k(xa, y_c), c < ncol
+    for (int64_t cb = (int64_t)warp * 4; cb < ncol; cb += NW * 4) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int k = lane; k < d; k += 32) {
+        const double xv = xa[k];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (cb + u < ncol) {
+            const double yv = ys[(cb + u) * d + k];
+            acc[u] = inner ? fma(xv, yv, acc[u]) : fma(xv - yv, xv - yv, acc[u]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+        if (lane == 0 && cb + u < ncol)
+          grow[cb + u] = inner ? static_from_inner(G.S, acc[u]) : static_from_sq(G.S, acc[u]);
+      }
+    }
+    __syncthreads();
+  };
+  // point-kernel values of the previous row at columns c0 .. c0 + n (difference)
+  double gp[CC + 1];
+  if (G.difference) {
+    if (wide) {
+      wide_row(xs);
+#pragma unroll
+      for (int k = 0; k <= CC; ++k) gp[k] = k <= n ? grow[c0 + k] : 0.0;
+      __syncthreads();
+    } else {
+#pragma unroll
+      for (int k = 0; k <= CC; ++k)
+        gp[k] = k <= n ? static_eval_f64(G.S, xs, ys + (c0 + k) * d, d) : 0.0;
+    }
+  }
   for (int64_t r = 0; r < T1; ++r) {
-    double a[CMAX];
+    double a[CC];
     if (G.difference) {
       const double *xa = xs + (r + 1) * d;
-      // G(r+1, c0 + k) for k = 1..n here; k = 0 from the previous thread
-      double g[CMAX + 1];
-      for (int k = 1; k <= n; ++k) g[k] = static_eval_f64(G.S, xa, ys + (c0 + k) * d, d);
-      const double last = n > 0 ? g[n] : 0.0;
-      const double up = __shfl_up_sync(0xffffffffu, last, 1);
-      if (lane == 31) smb[warp] = last;
-      __syncthreads();
-      if (t == 0)
-        g[0] = static_eval_f64(G.S, xa, ys, d);
-      else
-        g[0] = lane == 0 ? smb[warp - 1] : up;
+      double g[CC + 1];
+      if (wide) {
+        wide_row(xa);
+#pragma unroll
+        for (int k = 0; k <= CC; ++k) g[k] = k <= n ? grow[c0 + k] : 0.0;
+        __syncthreads();  // grow is rewritten next row
+      } else {
+        // G(r+1, c0 + k) for k = 1..n here; k = 0 from the previous thread
+#pragma unroll
+        for (int k = 1; k <= CC; ++k)
+          g[k] = k <= n ? static_eval_f64(G.S, xa, ys + (c0 + k) * d, d) : 0.0;
+        double last = 0.0;
+#pragma unroll
+        for (int k = 1; k <= CC; ++k)
+          if (k == n) last = g[k];
+        const double up = __shfl_up_sync(0xffffffffu, last, 1);
+        if (lane == 31) smb[warp] = last;
+        __syncthreads();
+        if (t == 0)
+          g[0] = static_eval_f64(G.S, xa, ys, d);
+        else
+          g[0] = lane == 0 ? smb[warp - 1] : up;
+      }
       // kernels.py:281: G[1:,1:] - G[:-1,1:] - G[1:,:-1] + G[:-1,:-1]
-      for (int k = 0; k < n; ++k) a[k] = g[k + 1] - gp[k + 1] - g[k] + gp[k];
-      for (int k = 0; k <= n; ++k) gp[k] = g[k];
+#pragma unroll
+      for (int k = 0; k < CC; ++k) a[k] = k < n ? g[k + 1] - gp[k + 1] - g[k] + gp[k] : 0.0;
+#pragma unroll
+      for (int k = 0; k <= CC; ++k) gp[k] = g[k];
+    } else if (wide) {
+      wide_row(xs + r * d);
+#pragma unroll
+      for (int k = 0; k < CC; ++k) a[k] = k < n ? grow[c0 + k] : 0.0;
+      __syncthreads();
     } else {
-      for (int k = 0; k < n; ++k)
-        a[k] = static_eval_f64(G.S, xs + r * d, ys + (c0 + k) * d, d);
+#pragma unroll
+      for (int k = 0; k < CC; ++k)
+        a[k] = k < n ? static_eval_f64(G.S, xs + r * d, ys + (c0 + k) * d, d) : 0.0;
     }
     // exclusive row prefix of the column accumulators (old values), levels 1..M-1
     double pre[VMAX];
-    for (int m = 0; m < VMAX; ++m) pre[m] = 0.0;
-    for (int m = 0; m < NV; ++m)
-      for (int k = 0; k < n; ++k) pre[m] += colacc[m * T2 + c0 + k];
+#pragma unroll
+    for (int m = 0; m < VMAX; ++m) {
+      pre[m] = 0.0;
+      if (REG || m < NV) {
+#pragma unroll
+        for (int k = 0; k < CC; ++k)
+          if (REG || k < n) pre[m] += CA(m, k);
+      }
+    }
     block_excl_scan(pre, NV, sm);
-    for (int k = 0; k < n; ++k) {
-      const int64_t c = c0 + k;
-      double Rprev = a[k];  // R_1
+#pragma unroll
+    for (int k = 0; k < CC; ++k) {
+      if (!REG && k >= n) break;
+      double Rprev = a[k];  // R_1 (0 beyond the own cells)
       lsum[0] += Rprev;
-      for (int m = 1; m < M; ++m) {  // R_{m+1} = A * S_m
-        const double R = a[k] * pre[m - 1];
-        lsum[m] += R;
-        double &acc = colacc[(m - 1) * T2 + c];
-        const double old = acc;
-        pre[m - 1] += old;
-        acc = old + Rprev;
-        Rprev = R;
+#pragma unroll
+      for (int m = 1; m < GEN_MAX_LEVELS; ++m) {  // R_{m+1} = A * S_m
+        if (m < M) {
+          const double R = a[k] * pre[m - 1];
+          lsum[m] += R;
+          double &acc = CA(m - 1, k);
+          const double old = acc;
+          pre[m - 1] += old;
+          acc = old + Rprev;
+          Rprev = R;
+        }
       }
     }
   }
   block_sum(lsum, M, sm, lv_out + 1);
   if (t == 0) lv_out[0] = 1.0;
   __syncthreads();
+}
+
+__device__ __noinline__ void cta_pair_levels(const Geo &G, const double *__restrict__ xs, int64_t lx,
+                                const double *__restrict__ ys, int64_t ly,
+                                double *__restrict__ colacc, double *sm, double *lv_out) {
+  const int64_t T1 = G.difference ? lx - 1 : lx, T2 = G.difference ? ly - 1 : ly;
+  if (G.M == 0 || T1 <= 0 || T2 <= 0) {
+    if (threadIdx.x == 0) {
+      lv_out[0] = 1.0;
+      for (int m = 1; m <= G.M; ++m) lv_out[m] = 0.0;
+    }
+    __syncthreads();
+    return;
+  }
+  const int64_t C = (T2 + RT - 1) / RT;
+  if (C <= 1)
+    cta_pair_levels_t<1>(G, xs, lx, ys, ly, colacc, sm, lv_out);
+  else if (C <= 2)
+    cta_pair_levels_t<2>(G, xs, lx, ys, ly, colacc, sm, lv_out);
+  else if (C <= 4)
+    cta_pair_levels_t<4>(G, xs, lx, ys, ly, colacc, sm, lv_out);
+  else if (C <= 8)
+    cta_pair_levels_t<8>(G, xs, lx, ys, ly, colacc, sm, lv_out);
+  else
+    cta_pair_levels_t<16>(G, xs, lx, ys, ly, colacc, sm, lv_out);
 }
 
 // --- the order-1 float64 Gram / self levels ---------------------------------
@@ -223,7 +343,8 @@ struct CertArgs {
   int64_t row_begin, rows;
   int norm;
   const double *diag_x, *diag_y;
-  const float *k1buf;  // FP32 level 1 per entry [row][ny], or null
+  const float2 *k1buf;  // per entry [row][ny]: (FP32 level 1, sum_m |k_m|), or null
+  int l1check;         // difference=True and n_levels >= 1: the exact-level-1 check
   double *K;
   int64_t ldk;
   double *levels;
@@ -231,51 +352,128 @@ struct CertArgs {
   int64_t slot;
 };
 
-// Pass 1 (every thread one entry at a time): the exact-level-1 check. Entries
-// whose FP32 level 1 deviates from the telescoped value by more than the
-// tolerance of their scale are marked NaN (with the mirror); the others are
-// corrected to the exact level 1.
-__global__ void cert_scan_kernel(CertArgs A) {
+// Pass 1: the exact-level-1 check. The four corner point-kernel values of
+// every entry are a small GEMM-shaped contraction over the channels, so CTAs
+// take tiles of SR rows x RT columns: the rows' first/last points are staged
+// in shared memory (SK channels at a time), every thread streams its column's
+// two corner points from the transposed corner arrays (coalesced) and keeps
+// 4 SR accumulators. Entries whose FP32 level 1 deviates from the telescoped
+// value by more than the tolerance of their scale are marked NaN (with the
+// mirror); the others are corrected to the exact level 1.
+constexpr int SR = 8, SK = 32;
+
+// Xc[(b * d + k) * n + i] = point (b ? L-1 : 0) of sequence i, channel k
+__global__ void corners_kernel(const double *__restrict__ X, int64_t n, int64_t L, int64_t d,
+                               double *__restrict__ Xc) {
+  const int64_t total = n * 2 * d;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t % n, rest = t / n, k = rest % d, b = rest / d;
+    Xc[t] = X[(i * L + (b ? L - 1 : 0)) * d + k];
+  }
+}
+
+template <bool INNER>
+__global__ void __launch_bounds__(RT) cert_scan_kernel(CertArgs A, const double *__restrict__ Xc,
+                                                       const double *__restrict__ Yc) {
+  __shared__ double xs[SR][2][SK];
   const Geo &G = A.G;
   const int M = G.M;
+  const int d = (int)G.d;
   const bool sym = A.symmetric;
-  const int64_t total = A.rows * G.ny;
-  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += nthr) {
-    const int64_t r = e / G.ny, j = e % G.ny;
-    const int64_t i = A.row_begin + r;
-    const int64_t row = sym ? i : r;
-    if (sym && j <= i) continue;  // the diagonal of K(X) is the self levels' own
-    double *kp = A.K + row * A.ldk + j;
-    const double v = *kp;
-    if (isnan(v)) continue;
-    const double k1e = exact_level1(G.S, G.X + i * G.lx * G.d, G.lx, G.Y + j * G.ly * G.d, G.ly,
-                                    (int)G.d);
-    const double delta = k1e - (double)A.k1buf[row * G.ny + j];
-    double scale = CERT_NOISE_RAW / CERT_NOISE * fabs(v), corr = delta;
-    if (A.norm != SK_NORM_NONE) {
-      const double *px = A.diag_x + i * (M + 1), *py = A.diag_y + j * (M + 1);
-      scale = sqrt(fabs(px[1] * py[1]));
-      if (A.norm == SK_NORM_LEVELWISE) {
-        const double den = sqrt((px[1] > 0.0 ? px[1] : 0.0) * (py[1] > 0.0 ? py[1] : 0.0));
-        corr = den > 0.0 ? delta / den / (double)(M + 1) : 0.0;
-      } else {
-        double sx = 0.0, sy = 0.0;
-        for (int m = 0; m <= M; ++m) {
-          sx += px[m];
-          sy += py[m];
-        }
-        corr = delta / sqrt(sx * sy);
+  const int64_t tiles_c = (G.ny + RT - 1) / RT, tiles = ((A.rows + SR - 1) / SR) * tiles_c;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t r0 = (tile / tiles_c) * SR, j = (tile % tiles_c) * RT + threadIdx.x;
+    const bool jv = j < G.ny;
+    double acc[SR][4];
+#pragma unroll
+    for (int r = 0; r < SR; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0.0;
+    for (int k0 = 0; k0 < d; k0 += SK) {
+      const int kn = min(SK, d - k0);
+      for (int e = threadIdx.x; e < SR * 2 * SK; e += RT) {
+        const int r = e / (2 * SK), b = (e / SK) & 1, k = e % SK;
+        const int64_t i = A.row_begin + r0 + r;
+        xs[r][b][k] = (r0 + r < A.rows && k < kn) ? Xc[(b * G.d + k0 + k) * G.nx + i] : 0.0;
       }
+      __syncthreads();
+      if (jv) {
+        for (int k = 0; k < kn; ++k) {
+          const double b0 = Yc[(k0 + k) * G.ny + j], b1 = Yc[(G.d + k0 + k) * G.ny + j];
+#pragma unroll
+          for (int r = 0; r < SR; ++r) {
+            const double a0 = xs[r][0][k], a1 = xs[r][1][k];
+            if (INNER) {
+              acc[r][0] = fma(a0, b0, acc[r][0]);
+              acc[r][1] = fma(a0, b1, acc[r][1]);
+              acc[r][2] = fma(a1, b0, acc[r][2]);
+              acc[r][3] = fma(a1, b1, acc[r][3]);
+            } else {
+              acc[r][0] = fma(a0 - b0, a0 - b0, acc[r][0]);
+              acc[r][1] = fma(a0 - b1, a0 - b1, acc[r][1]);
+              acc[r][2] = fma(a1 - b0, a1 - b0, acc[r][2]);
+              acc[r][3] = fma(a1 - b1, a1 - b1, acc[r][3]);
+            }
+          }
+        }
+      }
+      __syncthreads();
     }
-    const double nv = fabs(delta) > CERT_NOISE * scale
-                          ? __longlong_as_double(0x7ff8000000000000ll)
-                          : v + corr;
-    *kp = nv;
-    if (sym) A.K[j * A.ldk + i] = nv;
-    if (A.levels && !isnan(nv)) {
-      A.levels[(row * A.ldk + j) * (M + 1) + 1] = k1e;
-      if (sym) A.levels[(j * A.ldk + i) * (M + 1) + 1] = k1e;
+    if (!jv) continue;
+#pragma unroll
+    for (int r = 0; r < SR; ++r) {
+      if (r0 + r >= A.rows) break;
+      const int64_t i = A.row_begin + r0 + r;
+      const int64_t row = sym ? i : r0 + r;
+      if (sym && j <= i) continue;  // the diagonal of K(X) is the self levels' own
+      double *kp = A.K + row * A.ldk + j;
+      const double v = *kp;
+      // cancellation beyond what the FP32 levels resolve, or non-finite
+      const float2 kv = A.k1buf[row * G.ny + j];
+      const double lim = A.norm == SK_NORM_NONE
+                             ? (double)kv.y *
+                                   (G.S.kind == SK_LINEAR ? CERT_TAU_RAW_LINEAR : CERT_TAU_RAW)
+                             : CERT_TAU_NORM;
+      if (!(fabs(v) >= lim) || isinf(v)) {
+        *kp = __longlong_as_double(0x7ff8000000000000ll);
+        if (sym) A.K[j * A.ldk + i] = *kp;
+        continue;
+      }
+      if (!A.l1check) continue;
+      double k1e = 0.0;  // k(x_T,y_T') - k(x_0,y_T') - k(x_T,y_0) + k(x_0,y_0)
+      if (G.lx >= 2 && G.ly >= 2) {
+        if (INNER)
+          k1e = static_from_inner(G.S, acc[r][3]) - static_from_inner(G.S, acc[r][2]) -
+                static_from_inner(G.S, acc[r][1]) + static_from_inner(G.S, acc[r][0]);
+        else
+          k1e = static_from_sq(G.S, acc[r][3]) - static_from_sq(G.S, acc[r][2]) -
+                static_from_sq(G.S, acc[r][1]) + static_from_sq(G.S, acc[r][0]);
+      }
+      const double delta = k1e - (double)kv.x;
+      double scale = CERT_NOISE_RAW / CERT_NOISE * fabs(v), corr = delta;
+      if (A.norm != SK_NORM_NONE) {
+        const double *px = A.diag_x + i * (M + 1), *py = A.diag_y + j * (M + 1);
+        scale = sqrt(fabs(px[1] * py[1]));
+        if (A.norm == SK_NORM_LEVELWISE) {
+          const double den = sqrt((px[1] > 0.0 ? px[1] : 0.0) * (py[1] > 0.0 ? py[1] : 0.0));
+          corr = den > 0.0 ? delta / den / (double)(M + 1) : 0.0;
+        } else {
+          double sx = 0.0, sy = 0.0;
+          for (int m = 0; m <= M; ++m) {
+            sx += px[m];
+            sy += py[m];
+          }
+          corr = delta / sqrt(sx * sy);
+        }
+      }
+      const double nv = fabs(delta) > CERT_NOISE * scale
+                            ? __longlong_as_double(0x7ff8000000000000ll)
+                            : v + corr;
+      *kp = nv;
+      if (sym) A.K[j * A.ldk + i] = nv;
+      if (A.levels && !isnan(nv)) {
+        A.levels[(row * A.ldk + j) * (M + 1) + 1] = k1e;
+        if (sym) A.levels[(j * A.ldk + i) * (M + 1) + 1] = k1e;
+      }
     }
   }
 }
@@ -383,7 +581,9 @@ Geo geo(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny, in
 int64_t slot_doubles(int64_t lx, int64_t ly, const sk_kernel_config &c) {
   const int64_t L = std::max(lx, ly);
   const int64_t T = c.difference ? std::max<int64_t>(L - 1, 1) : std::max<int64_t>(L, 1);
-  return std::max(c.n_levels - 1, 1) * T;
+  // the row buffer of the wide (d >= 32) point-kernel evaluation, then the
+  // column accumulators of the long-row (more than 2 columns per thread) variant
+  return L + 2 + std::max(c.n_levels - 1, 1) * T;
 }
 
 int64_t grid_for(int64_t work, int64_t slot) {
@@ -432,15 +632,19 @@ int rowscan_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64
   if (!ws || ws_bytes < (size_t)(grid * A.slot * 8))
     return fail(SK_ERR_WORKSPACE, "workspace too small for the float64 row-scan kernel");
   A.scratch = (double *)ws;
-  gram_kernel<<<(unsigned)grid, RT, 0, st>>>(A);
+  SK_CHECK_CUDA(cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, YSTAGE_BYTES));
+  gram_kernel<<<(unsigned)grid, RT, YSTAGE_BYTES, st>>>(A);
   SK_CHECK_LAUNCH();
   return SK_OK;
 }
 
-size_t cert_workspace_bytes(int64_t lx, int64_t ly, const sk_kernel_config &c) {
+size_t cert_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int64_t d,
+                            const sk_kernel_config &c) {
   using namespace rowscan;
   const int64_t slot = slot_doubles(lx, ly, c);
-  return (size_t)grid_for(1ll << 40, slot) * slot * 8;
+  const size_t redo = (size_t)grid_for(1ll << 40, slot) * slot * 8;
+  const size_t corners = (size_t)(nx + ny) * 2 * d * 8;  // scan pass, before the redo
+  return std::max(redo, corners);
 }
 
 int cert_fixup(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny, int64_t ly,
@@ -457,23 +661,39 @@ int cert_fixup(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t
   A.norm = c.normalization;
   A.diag_x = diag_x;
   A.diag_y = diag_y;
-  A.k1buf = k1buf;
+  A.k1buf = reinterpret_cast<const float2 *>(k1buf);
   A.K = K;
   A.ldk = ldk;
   A.levels = levels;
   const int64_t total = A.rows * ny;
   if (total <= 0) return SK_OK;
-  if (k1buf && c.difference && c.n_levels >= 1) {
-    const unsigned g = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 8);
-    cert_scan_kernel<<<g, 256, 0, st>>>(A);
+  if (!ws || ws_bytes < cert_workspace_bytes(nx, lx, ny, ly, d, c))
+    return fail(SK_ERR_WORKSPACE, "workspace too small for the certification fix-up");
+  A.l1check = c.difference && c.n_levels >= 1;
+  if (k1buf) {
+    // transposed corner points of both roles (scan pass only; the redo reuses the space)
+    double *Xc = (double *)ws, *Yc = Xc + nx * 2 * d;
+    const int64_t tx = nx * 2 * d, ty = ny * 2 * d;
+    corners_kernel<<<(unsigned)std::min<int64_t>((tx + 255) / 256, sm_count() * 8), 256, 0, st>>>(
+        X, nx, lx, d, Xc);
+    SK_CHECK_LAUNCH();
+    corners_kernel<<<(unsigned)std::min<int64_t>((ty + 255) / 256, sm_count() * 8), 256, 0, st>>>(
+        symmetric ? X : Y, ny, ly, d, Yc);
+    SK_CHECK_LAUNCH();
+    const int64_t tiles = ((A.rows + SR - 1) / SR) * ((ny + RT - 1) / RT);
+    const unsigned g = (unsigned)std::min<int64_t>(tiles, (int64_t)sm_count() * 8);
+    const int k = c.static_spec.kind;
+    if (k == SK_LINEAR || k == SK_POLYNOMIAL)
+      cert_scan_kernel<true><<<g, RT, 0, st>>>(A, Xc, Yc);
+    else
+      cert_scan_kernel<false><<<g, RT, 0, st>>>(A, Xc, Yc);
     SK_CHECK_LAUNCH();
   }
   A.slot = slot_doubles(lx, ly, c);
   const int64_t grid = std::min<int64_t>(grid_for(1ll << 40, A.slot), (total + RT - 1) / RT);
-  if (!ws || ws_bytes < (size_t)(grid * A.slot * 8))
-    return fail(SK_ERR_WORKSPACE, "workspace too small for the certification fix-up");
   A.scratch = (double *)ws;
-  cert_redo_kernel<<<(unsigned)grid, RT, 0, st>>>(A);
+  SK_CHECK_CUDA(cudaFuncSetAttribute(cert_redo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, YSTAGE_BYTES));
+  cert_redo_kernel<<<(unsigned)grid, RT, YSTAGE_BYTES, st>>>(A);
   SK_CHECK_LAUNCH();
   return SK_OK;
 }
@@ -487,7 +707,8 @@ int cert_self_fixup(const double *X, int64_t n, int64_t l, int64_t d, const sk_k
   const int64_t grid = grid_for(n, slot);
   if (!ws || ws_bytes < (size_t)(grid * slot * 8))
     return fail(SK_ERR_WORKSPACE, "workspace too small for the self-level fix-up");
-  self_cert_kernel<<<(unsigned)grid, RT, 0, st>>>(G, out, (double *)ws, slot);
+  SK_CHECK_CUDA(cudaFuncSetAttribute(self_cert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, YSTAGE_BYTES));
+  self_cert_kernel<<<(unsigned)grid, RT, YSTAGE_BYTES, st>>>(G, out, (double *)ws, slot);
   SK_CHECK_LAUNCH();
   return SK_OK;
 }

@@ -688,12 +688,21 @@ def test_facade_diag(norm, kind, p):
         assert np.array_equal(got, np.diag(sk(X)))  # bitwise the Gram's own diagonal
 
 
+def _cancellation_flags(K, lv, kind, norm):
+    """The certification's cancellation rule (csrc/sk_common.cuh CERT_TAU_*), on the
+    FP32 K and level values: |K| < 0.05 normalised, |K| < tau sum_m |k_m| otherwise."""
+    if norm != "none":
+        return K.abs() < 0.05
+    tau = 1e-3 if kind == "linear" else 1e-2
+    return K.abs() < tau * lv.abs().sum(-1)
+
+
 def test_certification_flags_nothing_at_baseline_shapes():
     """The FP32 certification (sk_gram) recomputes only entries it cannot vouch for:
-    at BASELINE shapes (prefix blocks) no entry is flagged, i.e. the FP32 result is
-    the result — except c4's genuinely cancelling entries (linear kernel, |K| below
-    1e-3 of sum_m |k_m|: ~4e-4 of them). Checked with SK_FLAG_NO_FIXUP, which leaves
-    the NaN markers."""
+    at BASELINE shapes (prefix blocks) the cancellation rule flags nothing, i.e. the
+    FP32 result is the result — except c4's genuinely cancelling entries (linear
+    kernel, |K| below 1e-3 of sum_m |k_m|: ~4e-4 of them), which come back
+    float64-exact. SK_FLAG_NO_FIXUP returns the uncertified FP32 values."""
     from paper_2501_07145_b200 import _native
     from paper_2501_07145_b200.kernels import _self_levels_t, gram_block
     for (n, L, d, M, p, kind, norm) in ((64, 50, 3, 5, 1, "rbf", "levelwise"),
@@ -707,21 +716,21 @@ def test_certification_flags_nothing_at_baseline_shapes():
                            normalization=norm)
         dx = dy = None
         if norm != "none":
-            dx = _self_levels_t(X, cfg, "fp32", flags=_native.SK_FLAG_NO_FIXUP)
-            dy = _self_levels_t(Y, cfg, "fp32", flags=_native.SK_FLAG_NO_FIXUP)
-            assert bool(torch.isfinite(dx).all()) and bool(torch.isfinite(dy).all())
-        K, _ = gram_block(X, Y, cfg, diag_x=dx, diag_y=dy, flags=_native.SK_FLAG_NO_FIXUP)
-        limit = 2e-3 * K.numel() if kind == "linear" else 0
-        assert int(torch.isnan(K).sum()) <= limit, (n, L, d, M, kind, norm)
-        if kind == "linear":  # the flagged entries come back float64-exact
+            dx = _self_levels_t(X, cfg, "fp32")
+            dy = _self_levels_t(Y, cfg, "fp32")
+        K0, lv = gram_block(X, Y, cfg, diag_x=dx, diag_y=dy, want_levels=True,
+                            flags=_native.SK_FLAG_NO_FIXUP)
+        flagged = _cancellation_flags(K0, lv, kind, norm)
+        limit = 2e-3 * K0.numel() if kind == "linear" else 0
+        assert int(flagged.sum()) <= limit, (n, L, d, M, kind, norm)
+        if flagged.any():  # the flagged entries come back float64-exact
             Kf = sig_kernel_gram(X, Y, cfg=cfg)
             K64 = sig_kernel_gram(X, Y, cfg=cfg, precision="fp64")
-            nan = torch.isnan(K)
-            assert torch.allclose(Kf[nan], K64[nan], rtol=1e-12, atol=0)
+            assert torch.allclose(Kf[flagged], K64[flagged], rtol=1e-12, atol=0)
 
 
 def test_certification_fixup_recomputes_in_float64():
-    """Entries the FP32 epilogue flags are the float64 values after the fix-up: a
+    """Entries the certification flags are the float64 values after the fix-up: a
     cancelling levelwise case (seed 28 of the sweep: entry 2.5e-3)."""
     from paper_2501_07145_b200 import _native
     from paper_2501_07145_b200.kernels import gram_block
@@ -730,8 +739,8 @@ def test_certification_fixup_recomputes_in_float64():
     Y = gen_brownian(4, 63, 2, SeedStream(28, ("y",))).data
     cfg = KernelConfig(static=StaticKernelSpec(**sp), n_levels=8, normalization="levelwise")
     Xt, Yt = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
-    K0, _ = gram_block(Xt, Yt, cfg, flags=_native.SK_FLAG_NO_FIXUP)
-    flagged = torch.isnan(K0).cpu().numpy()
+    K0, lv = gram_block(Xt, Yt, cfg, flags=_native.SK_FLAG_NO_FIXUP, want_levels=True)
+    flagged = _cancellation_flags(K0, lv, "rbf", "levelwise").cpu().numpy()
     assert flagged.any()
     K = sig_kernel_gram(X, Y, cfg=cfg)
     K64 = sig_kernel_gram(X, Y, cfg=cfg, precision="fp64")

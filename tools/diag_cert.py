@@ -44,3 +44,15 @@ print("|K| / sum|k_m|: min %.3e median %.3e" % (np.nanmin(np.abs(Kc) / s), np.na
 r = np.abs(lv.sum(-1)) / s  # from the level values (K itself is NaN where flagged)
 for t in (1e-2, 3e-3, 1e-3, 3e-4):
     print("fraction with |K| < %.0e sum|k_m|: %.2e" % (t, float(np.mean(r < t))))
+# FP32 error (after the exact-level-1 correction) against float64, bucketed by
+# the cancellation ratio |K| / sum_m |k_m| the certification rule uses
+if norm == "none":
+    K64 = gram_block(X, Y, cfg, precision="fp64")[0].cpu().numpy()
+    K32c = lv.sum(-1) - lv[..., 1] + k1
+    err = np.abs(K32c - K64) / np.abs(K64)
+    r = np.abs(lv.sum(-1)) / s
+    for lo, hi in ((0, 1e-4), (1e-4, 3e-4), (3e-4, 1e-3), (1e-3, 1e-2), (1e-2, 10)):
+        m = (r >= lo) & (r < hi)
+        if m.any():
+            print("ratio [%.0e, %.0e): %d entries, FP32 rel err max %.2e median %.2e"
+                  % (lo, hi, int(m.sum()), err[m].max(), np.median(err[m])))
