@@ -26,8 +26,23 @@ constexpr int RT = 256;            // threads per CTA
 constexpr int NW = RT / 32;
 constexpr int CMAX = 16;           // columns per thread: T2 <= 4096 (cta_pair_levels_t)
 constexpr int VMAX = GEN_MAX_LEVELS - 1;  // scanned levels (1..M-1)
-constexpr int YSTAGE_BYTES = 96 * 1024;   // dynamic shared memory for the y staging
+constexpr int YSTAGE_BYTES = 96 * 1024;   // dynamic shared memory: y staging / wide blocks
+constexpr int WR = 16, KW = 8;            // wide path: point-kernel rows per block, channels per stage
+constexpr int WIDE_COLS = (YSTAGE_BYTES / 8 - WR * KW - RT * KW) / WR;  // max columns of a block
 __device__ __forceinline__ int64_t ystage_doubles() { return YSTAGE_BYTES / 8; }
+
+// The static kernel evaluations of this file are out-of-line calls: inlined
+// into every unrolled instance they made ptxas take over ten minutes.
+__device__ __noinline__ double kf_eval(const StaticF64 &S, const double *x, const double *y,
+                                       int d) {
+  return static_eval_f64(S, x, y, d);
+}
+__device__ __noinline__ double kf_sq(const StaticF64 &S, double sq) {
+  return static_from_sq(S, sq);
+}
+__device__ __noinline__ double kf_inner(const StaticF64 &S, double xy) {
+  return static_from_inner(S, xy);
+}
 
 struct Geo {
   const double *X, *Y;
@@ -38,15 +53,16 @@ struct Geo {
 
 // Block-wide exclusive prefix of nv values per thread (in place); every thread
 // must call it. sm: NW * VMAX doubles.
-__device__ __forceinline__ void block_excl_scan(double (&v)[VMAX], int nv, double *sm) {
+template <int NVB>
+__device__ __forceinline__ void block_excl_scan(double (&v)[NVB], int nv, double *sm) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double inc[VMAX];
+  double inc[NVB];
 #pragma unroll
-  for (int k = 0; k < VMAX; ++k) inc[k] = v[k];
+  for (int k = 0; k < NVB; ++k) inc[k] = v[k];
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
 #pragma unroll
-    for (int k = 0; k < VMAX; ++k) {
+    for (int k = 0; k < NVB; ++k) {
       if (k < nv) {
         const double u = __shfl_up_sync(0xffffffffu, inc[k], o);
         if (lane >= o) inc[k] += u;
@@ -83,12 +99,62 @@ __device__ __forceinline__ void block_sum(const double *v, int n, double *sm, do
   __syncthreads();
 }
 
+// Point-kernel rows gb .. gb+rb of the pair into gblk[r * WIDE_COLS + c],
+// c < ncol: a float64 block product of the rows' x points and all y points,
+// KW channels per shared-memory stage (thread = column, WR accumulators).
+__device__ __noinline__ void wide_block(const Geo &G, const double *__restrict__ xs,
+                                        const double *__restrict__ ys, int64_t gb, int rb,
+                                        int64_t ncol, double *gblk) {
+  const int t = threadIdx.x, d = (int)G.d;
+  const bool inner = G.S.kind == SK_LINEAR || G.S.kind == SK_POLYNOMIAL;
+  double *xt = gblk + WR * WIDE_COLS, *yt = xt + WR * KW;
+  double xx[WR];
+  for (int cb = 0; cb < ncol; cb += RT) {  // columns c = cb + t
+    const int c = cb + t;
+    double acc[WR];
+#pragma unroll
+    for (int r = 0; r < WR; ++r) acc[r] = xx[r] = 0.0;
+    double yy = 0.0;
+    for (int k0 = 0; k0 < d; k0 += KW) {
+      const int kn = d - k0 < KW ? d - k0 : KW;
+      __syncthreads();
+      for (int e = t; e < WR * KW; e += RT) {
+        const int r = e / KW, k = e % KW;
+        xt[e] = (r < rb && k < kn) ? xs[(gb + r) * d + k0 + k] : 0.0;
+      }
+      for (int e = t; e < RT * KW; e += RT) {  // y rows cb..cb+RT, KW channels
+        const int cc = e / KW, k = e % KW;
+        yt[e] = (cb + cc < ncol && k < kn) ? ys[(int64_t)(cb + cc) * d + k0 + k] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < KW; ++k) {
+        const double yv = yt[t * KW + k];
+        yy = fma(yv, yv, yy);
+#pragma unroll
+        for (int r = 0; r < WR; ++r) {
+          const double xv = xt[r * KW + k];
+          acc[r] = fma(xv, yv, acc[r]);
+          xx[r] = fma(xv, xv, xx[r]);
+        }
+      }
+    }
+    if (c < ncol) {
+#pragma unroll
+      for (int r = 0; r < WR; ++r)
+        gblk[r * WIDE_COLS + c] =
+            inner ? kf_inner(G.S, acc[r]) : kf_sq(G.S, xx[r] + yy - 2.0 * acc[r]);
+    }
+  }
+  __syncthreads();
+}
+
 // Level values k_0..k_M of the pair (xs: lx points, ys: ly points) into
 // lv_out[0..M] (shared memory, written by thread 0; visible after return).
 // colacc: this CTA's scratch slice (slot_doubles). All threads call it.
 // CC: compile-time columns per thread (>= ceil(T2 / RT)); every per-thread
 // array is indexed by unrolled compile-time loops so it stays in registers.
-template <int CC>
+template <int CC, int MB>
 __device__ __noinline__ void cta_pair_levels_t(const Geo &G, const double *__restrict__ xs, int64_t lx,
                                   const double *ys, int64_t ly, double *__restrict__ colacc,
                                   double *sm, double *lv_out) {
@@ -102,7 +168,8 @@ __device__ __noinline__ void cta_pair_levels_t(const Geo &G, const double *__res
   // column accumulators of levels 1..M-1 for the own columns: registers for
   // CC <= 2 (every loop unrolled), else the scratch slice (rows of T2 doubles)
   constexpr bool REG = CC <= 2;
-  double ca[REG ? VMAX : 1][REG ? CC : 1];
+  constexpr int VB = MB - 1;  // level bound of this instance (M <= MB)
+  double ca[REG ? VB : 1][REG ? CC : 1];
   double *cmem = colacc + T2 + 2;  // after the row buffer
   auto CA = [&](int m, int k) -> double & {
     if constexpr (REG) return ca[m][k];
@@ -110,7 +177,7 @@ __device__ __noinline__ void cta_pair_levels_t(const Geo &G, const double *__res
   };
   if constexpr (REG) {
 #pragma unroll
-    for (int m = 0; m < VMAX; ++m)
+    for (int m = 0; m < VB; ++m)
 #pragma unroll
       for (int k = 0; k < CC; ++k) ca[m][k] = 0.0;
   } else {
@@ -119,9 +186,9 @@ __device__ __noinline__ void cta_pair_levels_t(const Geo &G, const double *__res
       for (int k = 0; k < CC; ++k)
         if (k < n) CA(m, k) = 0.0;
   }
-  double lsum[GEN_MAX_LEVELS];
+  double lsum[MB];
 #pragma unroll
-  for (int m = 0; m < GEN_MAX_LEVELS; ++m) lsum[m] = 0.0;
+  for (int m = 0; m < MB; ++m) lsum[m] = 0.0;
   double *smb = sm + NW * VMAX;  // warp-boundary point-kernel values
   // d >= 32: a row's point-kernel values are formed warp-cooperatively (lanes
   // over channels: coalesced reads of every y point) into a row buffer in the
@@ -157,71 +224,18 @@ __device__ __noinline__ void cta_pair_levels_t(const Geo &G, const double *__res
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
         if (lane == 0 && cb + u < ncol)
-          grow[cb + u] = inner ? static_from_inner(G.S, acc[u]) : static_from_sq(G.S, acc[u]);
+          grow[cb + u] = inner ? kf_inner(G.S, acc[u]) : kf_sq(G.S, acc[u]);
       }
     }
     __syncthreads();
   };
-  // point-kernel values of the previous row at columns c0 .. c0 + n (difference)
-  double gp[CC + 1];
-  if (G.difference) {
-    if (wide) {
-      wide_row(xs);
-#pragma unroll
-      for (int k = 0; k <= CC; ++k) gp[k] = k <= n ? grow[c0 + k] : 0.0;
-      __syncthreads();
-    } else {
-#pragma unroll
-      for (int k = 0; k <= CC; ++k)
-        gp[k] = k <= n ? static_eval_f64(G.S, xs, ys + (c0 + k) * d, d) : 0.0;
-    }
-  }
-  for (int64_t r = 0; r < T1; ++r) {
-    double a[CC];
-    if (G.difference) {
-      const double *xa = xs + (r + 1) * d;
-      double g[CC + 1];
-      if (wide) {
-        wide_row(xa);
-#pragma unroll
-        for (int k = 0; k <= CC; ++k) g[k] = k <= n ? grow[c0 + k] : 0.0;
-        __syncthreads();  // grow is rewritten next row
-      } else {
-        // G(r+1, c0 + k) for k = 1..n here; k = 0 from the previous thread
-#pragma unroll
-        for (int k = 1; k <= CC; ++k)
-          g[k] = k <= n ? static_eval_f64(G.S, xa, ys + (c0 + k) * d, d) : 0.0;
-        double last = 0.0;
-#pragma unroll
-        for (int k = 1; k <= CC; ++k)
-          if (k == n) last = g[k];
-        const double up = __shfl_up_sync(0xffffffffu, last, 1);
-        if (lane == 31) smb[warp] = last;
-        __syncthreads();
-        if (t == 0)
-          g[0] = static_eval_f64(G.S, xa, ys, d);
-        else
-          g[0] = lane == 0 ? smb[warp - 1] : up;
-      }
-      // kernels.py:281: G[1:,1:] - G[:-1,1:] - G[1:,:-1] + G[:-1,:-1]
-#pragma unroll
-      for (int k = 0; k < CC; ++k) a[k] = k < n ? g[k + 1] - gp[k + 1] - g[k] + gp[k] : 0.0;
-#pragma unroll
-      for (int k = 0; k <= CC; ++k) gp[k] = g[k];
-    } else if (wide) {
-      wide_row(xs + r * d);
-#pragma unroll
-      for (int k = 0; k < CC; ++k) a[k] = k < n ? grow[c0 + k] : 0.0;
-      __syncthreads();
-    } else {
-#pragma unroll
-      for (int k = 0; k < CC; ++k)
-        a[k] = k < n ? static_eval_f64(G.S, xs + r * d, ys + (c0 + k) * d, d) : 0.0;
-    }
+  // one row of the level recursion (R_1 = A, R_{m+1} = A * S_m) from this
+  // thread's cells a[0..n)
+  auto dp_row = [&](const double (&a)[CC]) {
     // exclusive row prefix of the column accumulators (old values), levels 1..M-1
-    double pre[VMAX];
+    double pre[VB];
 #pragma unroll
-    for (int m = 0; m < VMAX; ++m) {
+    for (int m = 0; m < VB; ++m) {
       pre[m] = 0.0;
       if (REG || m < NV) {
 #pragma unroll
@@ -230,14 +244,31 @@ __device__ __noinline__ void cta_pair_levels_t(const Geo &G, const double *__res
       }
     }
     block_excl_scan(pre, NV, sm);
+    if constexpr (REG) {
 #pragma unroll
-    for (int k = 0; k < CC; ++k) {
-      if (!REG && k >= n) break;
-      double Rprev = a[k];  // R_1 (0 beyond the own cells)
-      lsum[0] += Rprev;
+      for (int k = 0; k < CC; ++k) {
+        double Rprev = a[k];  // R_1 (0 beyond the own cells)
+        lsum[0] += Rprev;
 #pragma unroll
-      for (int m = 1; m < GEN_MAX_LEVELS; ++m) {  // R_{m+1} = A * S_m
-        if (m < M) {
+        for (int m = 1; m < MB; ++m) {  // R_{m+1} = A * S_m
+          if (m < M) {
+            const double R = a[k] * pre[m - 1];
+            lsum[m] += R;
+            double &acc = CA(m - 1, k);
+            const double old = acc;
+            pre[m - 1] += old;
+            acc = old + Rprev;
+            Rprev = R;
+          }
+        }
+      }
+    } else {  // long rows: runtime loops (the column state is in the scratch slice anyway)
+#pragma unroll 1
+      for (int k = 0; k < n; ++k) {
+        double Rprev = a[k];
+        lsum[0] += Rprev;
+#pragma unroll 1
+        for (int m = 1; m < M; ++m) {
           const double R = a[k] * pre[m - 1];
           lsum[m] += R;
           double &acc = CA(m - 1, k);
@@ -247,6 +278,100 @@ __device__ __noinline__ void cta_pair_levels_t(const Geo &G, const double *__res
           Rprev = R;
         }
       }
+    }
+  };
+  // point-kernel values of the previous row at columns c0 .. c0 + n (difference)
+  double gp[CC + 1];
+  if (wide && ncol <= WIDE_COLS) {
+    // Row blocks of WR point-kernel rows at a time: a float64 block product of
+    // the block's x points and all y points, KW channels per shared-memory
+    // stage (thread = column, WR accumulators), into gblk[WR][ncol]; the
+    // recursion then reads its rows from shared memory.
+    double *gblk = ystage;
+    const int64_t nrows = G.difference ? lx : T1;  // point-kernel rows
+    for (int64_t gb = 0; gb < nrows; gb += WR) {
+      const int rb = nrows - gb < WR ? (int)(nrows - gb) : WR;
+      wide_block(G, xs, ys, gb, rb, ncol, gblk);
+      __syncthreads();
+      for (int r = 0; r < rb; ++r) {
+        const double *grow_s = gblk + r * WIDE_COLS;
+        double a[CC];
+        if (G.difference) {
+          double g[CC + 1];
+#pragma unroll
+          for (int k = 0; k <= CC; ++k) g[k] = k <= n ? grow_s[c0 + k] : 0.0;
+          if (gb + r > 0) {
+            // kernels.py:281: G[1:,1:] - G[:-1,1:] - G[1:,:-1] + G[:-1,:-1]
+#pragma unroll
+            for (int k = 0; k < CC; ++k)
+              a[k] = k < n ? g[k + 1] - gp[k + 1] - g[k] + gp[k] : 0.0;
+          }
+#pragma unroll
+          for (int k = 0; k <= CC; ++k) gp[k] = g[k];
+          if (gb + r == 0) continue;  // point row 0: no increment row yet (CTA-uniform)
+        } else {
+#pragma unroll
+          for (int k = 0; k < CC; ++k) a[k] = k < n ? grow_s[c0 + k] : 0.0;
+        }
+        dp_row(a);
+      }
+    }
+  } else {
+    if (G.difference) {
+      if (wide) {
+        wide_row(xs);
+#pragma unroll
+        for (int k = 0; k <= CC; ++k) gp[k] = k <= n ? grow[c0 + k] : 0.0;
+        __syncthreads();
+      } else {
+#pragma unroll
+        for (int k = 0; k <= CC; ++k)
+          gp[k] = k <= n ? kf_eval(G.S, xs, ys + (c0 + k) * d, d) : 0.0;
+      }
+    }
+    for (int64_t r = 0; r < T1; ++r) {
+      double a[CC];
+      if (G.difference) {
+        const double *xa = xs + (r + 1) * d;
+        double g[CC + 1];
+        if (wide) {
+          wide_row(xa);
+#pragma unroll
+          for (int k = 0; k <= CC; ++k) g[k] = k <= n ? grow[c0 + k] : 0.0;
+          __syncthreads();  // grow is rewritten next row
+        } else {
+          // G(r+1, c0 + k) for k = 1..n here; k = 0 from the previous thread
+#pragma unroll
+          for (int k = 1; k <= CC; ++k)
+            g[k] = k <= n ? kf_eval(G.S, xa, ys + (c0 + k) * d, d) : 0.0;
+          double last = 0.0;
+#pragma unroll
+          for (int k = 1; k <= CC; ++k)
+            if (k == n) last = g[k];
+          const double up = __shfl_up_sync(0xffffffffu, last, 1);
+          if (lane == 31) smb[warp] = last;
+          __syncthreads();
+          if (t == 0)
+            g[0] = kf_eval(G.S, xa, ys, d);
+          else
+            g[0] = lane == 0 ? smb[warp - 1] : up;
+        }
+        // kernels.py:281: G[1:,1:] - G[:-1,1:] - G[1:,:-1] + G[:-1,:-1]
+#pragma unroll
+        for (int k = 0; k < CC; ++k) a[k] = k < n ? g[k + 1] - gp[k + 1] - g[k] + gp[k] : 0.0;
+#pragma unroll
+        for (int k = 0; k <= CC; ++k) gp[k] = g[k];
+      } else if (wide) {
+        wide_row(xs + r * d);
+#pragma unroll
+        for (int k = 0; k < CC; ++k) a[k] = k < n ? grow[c0 + k] : 0.0;
+        __syncthreads();
+      } else {
+#pragma unroll
+        for (int k = 0; k < CC; ++k)
+          a[k] = k < n ? kf_eval(G.S, xs + r * d, ys + (c0 + k) * d, d) : 0.0;
+      }
+      dp_row(a);
     }
   }
   block_sum(lsum, M, sm, lv_out + 1);
@@ -266,17 +391,20 @@ __device__ __noinline__ void cta_pair_levels(const Geo &G, const double *__restr
     __syncthreads();
     return;
   }
+  // instances: columns per thread x level bound (M <= 4 / 8 / 16)
   const int64_t C = (T2 + RT - 1) / RT;
-  if (C <= 1)
-    cta_pair_levels_t<1>(G, xs, lx, ys, ly, colacc, sm, lv_out);
-  else if (C <= 2)
-    cta_pair_levels_t<2>(G, xs, lx, ys, ly, colacc, sm, lv_out);
-  else if (C <= 4)
-    cta_pair_levels_t<4>(G, xs, lx, ys, ly, colacc, sm, lv_out);
-  else if (C <= 8)
-    cta_pair_levels_t<8>(G, xs, lx, ys, ly, colacc, sm, lv_out);
-  else
-    cta_pair_levels_t<16>(G, xs, lx, ys, ly, colacc, sm, lv_out);
+  const int M = G.M;
+#define SK_RS(CCV, MBV) cta_pair_levels_t<CCV, MBV>(G, xs, lx, ys, ly, colacc, sm, lv_out)
+  if (C <= 1) {
+    if (M <= 4) SK_RS(1, 4); else if (M <= 8) SK_RS(1, 8); else SK_RS(1, 16);
+  } else if (C <= 2) {
+    if (M <= 4) SK_RS(2, 4); else if (M <= 8) SK_RS(2, 8); else SK_RS(2, 16);
+  } else if (C <= 8) {
+    if (M <= 8) SK_RS(8, 8); else SK_RS(8, 16);
+  } else {
+    SK_RS(16, 16);
+  }
+#undef SK_RS
 }
 
 // --- the order-1 float64 Gram / self levels ---------------------------------
@@ -294,7 +422,7 @@ struct GramArgs {
   int64_t slot;  // doubles of scratch per CTA
 };
 
-__global__ void __launch_bounds__(RT) gram_kernel(GramArgs A) {
+__global__ void __launch_bounds__(RT, 2) gram_kernel(GramArgs A) {
   __shared__ double sm[NW * (VMAX + 1) + NW + 2 * (GEN_MAX_LEVELS + 1)];
   double *lv = sm + NW * (VMAX + 1) + NW;
   const Geo &G = A.G;
@@ -442,11 +570,11 @@ __global__ void __launch_bounds__(RT) cert_scan_kernel(CertArgs A, const double 
       double k1e = 0.0;  // k(x_T,y_T') - k(x_0,y_T') - k(x_T,y_0) + k(x_0,y_0)
       if (G.lx >= 2 && G.ly >= 2) {
         if (INNER)
-          k1e = static_from_inner(G.S, acc[r][3]) - static_from_inner(G.S, acc[r][2]) -
-                static_from_inner(G.S, acc[r][1]) + static_from_inner(G.S, acc[r][0]);
+          k1e = kf_inner(G.S, acc[r][3]) - kf_inner(G.S, acc[r][2]) -
+                kf_inner(G.S, acc[r][1]) + kf_inner(G.S, acc[r][0]);
         else
-          k1e = static_from_sq(G.S, acc[r][3]) - static_from_sq(G.S, acc[r][2]) -
-                static_from_sq(G.S, acc[r][1]) + static_from_sq(G.S, acc[r][0]);
+          k1e = kf_sq(G.S, acc[r][3]) - kf_sq(G.S, acc[r][2]) -
+                kf_sq(G.S, acc[r][1]) + kf_sq(G.S, acc[r][0]);
       }
       const double delta = k1e - (double)kv.x;
       double scale = CERT_NOISE_RAW / CERT_NOISE * fabs(v), corr = delta;
@@ -480,7 +608,7 @@ __global__ void __launch_bounds__(RT) cert_scan_kernel(CertArgs A, const double 
 
 // Pass 2: CTAs stride over the entries RT at a time and recompute every NaN
 // entry in float64, one pair (plus both self levels when normalised) per CTA.
-__global__ void __launch_bounds__(RT) cert_redo_kernel(CertArgs A) {
+__global__ void __launch_bounds__(RT, 2) cert_redo_kernel(CertArgs A) {
   __shared__ double sm[NW * (VMAX + 1) + NW + 3 * (GEN_MAX_LEVELS + 1)];
   __shared__ int64_t list[RT];
   __shared__ int cnt;
@@ -530,7 +658,7 @@ __global__ void __launch_bounds__(RT) cert_redo_kernel(CertArgs A) {
 }
 
 // Self levels: level 1 -> exact; noisy, negative or non-finite -> float64.
-__global__ void __launch_bounds__(RT) self_cert_kernel(Geo G, double *out, double *scratch,
+__global__ void __launch_bounds__(RT, 2) self_cert_kernel(Geo G, double *out, double *scratch,
                                                        int64_t slot) {
   __shared__ double sm[NW * (VMAX + 1) + NW + (GEN_MAX_LEVELS + 1)];
   __shared__ int redo;

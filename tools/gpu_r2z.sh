@@ -1,0 +1,8 @@
+set -x
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -4
+timeout 300 python tools/diag_fp64_pair.py c4 2>&1 | tail -3
+timeout 300 python tools/diag_fp64_pair.py c3 2>&1 | tail -3
+timeout 300 python tools/devtime.py c4 4096 fp32 2 nofix 2>&1 | tail -1
+timeout 300 python tools/devtime.py c4 4096 fp32 2 2>&1 | tail -1
+timeout 900 python tools/bulk_parity.py c4 64 3 2>&1 | tail -1
+timeout 300 python tools/devtime.py c3 256 fp64 2 2>&1 | tail -1
