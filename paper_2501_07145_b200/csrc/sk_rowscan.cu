@@ -27,7 +27,7 @@ constexpr int NW = RT / 32;
 constexpr int CMAX = 16;           // columns per thread: T2 <= 4096 (cta_pair_levels_t)
 constexpr int VMAX = GEN_MAX_LEVELS - 1;  // scanned levels (1..M-1)
 constexpr int YSTAGE_BYTES = 96 * 1024;   // dynamic shared memory: y staging / wide blocks
-constexpr int WR = 16, KW = 8;            // wide path: point-kernel rows per block, channels per stage
+constexpr int WR = 16, KW = 16;           // wide path: point-kernel rows per block, channels per stage
 constexpr int WIDE_COLS = (YSTAGE_BYTES / 8 - WR * KW - RT * KW) / WR;  // max columns of a block
 __device__ __forceinline__ int64_t ystage_doubles() { return YSTAGE_BYTES / 8; }
 
@@ -43,6 +43,10 @@ __device__ __noinline__ double kf_sq(const StaticF64 &S, double sq) {
 __device__ __noinline__ double kf_inner(const StaticF64 &S, double xy) {
   return static_from_inner(S, xy);
 }
+// out[r * WIDE_COLS] = k(v[r]) for a block column (one call for WR / 2 values)
+constexpr int WR_ = 16;
+__device__ __noinline__ void kf_many(const StaticF64 &S, bool inner, const double (&v)[WR_ / 2],
+                                     double *out);
 
 struct Geo {
   const double *X, *Y;
@@ -99,51 +103,91 @@ __device__ __forceinline__ void block_sum(const double *v, int n, double *sm, do
   __syncthreads();
 }
 
+static_assert(WR == WR_, "kf_many block height");
+__device__ __noinline__ void kf_many(const StaticF64 &S, bool inner, const double (&v)[WR_ / 2],
+                                     double *out) {
+  for (int r = 0; r < WR_ / 2; ++r)
+    out[r * WIDE_COLS] = inner ? static_from_inner(S, v[r]) : static_from_sq(S, v[r]);
+}
+
 // Point-kernel rows gb .. gb+rb of the pair into gblk[r * WIDE_COLS + c],
 // c < ncol: a float64 block product of the rows' x points and all y points,
 // KW channels per shared-memory stage (thread = column, WR accumulators).
 __device__ __noinline__ void wide_block(const Geo &G, const double *__restrict__ xs,
                                         const double *__restrict__ ys, int64_t gb, int rb,
                                         int64_t ncol, double *gblk) {
+  // two threads per column, RPT rows each: 128 columns per pass
+  constexpr int RPT = WR / 2, CPP = RT / 2;
   const int t = threadIdx.x, d = (int)G.d;
+  const int ct = t >> 1, r0 = (t & 1) * RPT;
   const bool inner = G.S.kind == SK_LINEAR || G.S.kind == SK_POLYNOMIAL;
   double *xt = gblk + WR * WIDE_COLS, *yt = xt + WR * KW;
-  double xx[WR];
-  for (int cb = 0; cb < ncol; cb += RT) {  // columns c = cb + t
-    const int c = cb + t;
-    double acc[WR];
+  for (int cb = 0; cb < ncol; cb += CPP) {  // columns c = cb + ct
+    const int c = cb + ct;
+    double acc[WR_ / 2], xx[WR_ / 2];
 #pragma unroll
-    for (int r = 0; r < WR; ++r) acc[r] = xx[r] = 0.0;
+    for (int r = 0; r < RPT; ++r) acc[r] = xx[r] = 0.0;
     double yy = 0.0;
-    for (int k0 = 0; k0 < d; k0 += KW) {
+    // stage loads prefetched one stage ahead into registers (the staging was
+    // latency-bound: every shared store waited for its global load)
+    constexpr int XE = (WR * KW + RT - 1) / RT, YE = (CPP * KW + RT - 1) / RT;
+    double xr[XE], yr[YE];
+    auto fetch = [&](int k0) {
       const int kn = d - k0 < KW ? d - k0 : KW;
-      __syncthreads();
-      for (int e = t; e < WR * KW; e += RT) {
-        const int r = e / KW, k = e % KW;
-        xt[e] = (r < rb && k < kn) ? xs[(gb + r) * d + k0 + k] : 0.0;
-      }
-      for (int e = t; e < RT * KW; e += RT) {  // y rows cb..cb+RT, KW channels
-        const int cc = e / KW, k = e % KW;
-        yt[e] = (cb + cc < ncol && k < kn) ? ys[(int64_t)(cb + cc) * d + k0 + k] : 0.0;
-      }
-      __syncthreads();
 #pragma unroll
-      for (int k = 0; k < KW; ++k) {
-        const double yv = yt[t * KW + k];
-        yy = fma(yv, yv, yy);
+      for (int u = 0; u < XE; ++u) {
+        const int e = t + u * RT, r = e / KW, k = e % KW;
+        xr[u] = (e < WR * KW && r < rb && k < kn) ? xs[(gb + r) * d + k0 + k] : 0.0;
+      }
 #pragma unroll
-        for (int r = 0; r < WR; ++r) {
-          const double xv = xt[r * KW + k];
-          acc[r] = fma(xv, yv, acc[r]);
-          xx[r] = fma(xv, xv, xx[r]);
+      for (int u = 0; u < YE; ++u) {
+        const int e = t + u * RT, cc = e / KW, k = e % KW;
+        yr[u] = (e < CPP * KW && cb + cc < ncol && k < kn) ? ys[(int64_t)(cb + cc) * d + k0 + k]
+                                                           : 0.0;
+      }
+    };
+    fetch(0);
+    for (int k0 = 0; k0 < d; k0 += KW) {
+      __syncthreads();  // the previous stage's readers are done
+#pragma unroll
+      for (int u = 0; u < XE; ++u)
+        if (t + u * RT < WR * KW) xt[t + u * RT] = xr[u];
+#pragma unroll
+      for (int u = 0; u < YE; ++u)
+        if (t + u * RT < CPP * KW) yt[t + u * RT] = yr[u];
+      __syncthreads();
+      if (k0 + KW < d) fetch(k0 + KW);
+      if (inner) {
+#pragma unroll
+        for (int k = 0; k < KW; ++k) {
+          const double yv = yt[ct * KW + k];
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) acc[r] = fma(xt[(r0 + r) * KW + k], yv, acc[r]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < KW; ++k) {
+          const double yv = yt[ct * KW + k];
+          yy = fma(yv, yv, yy);
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            const double xv = xt[(r0 + r) * KW + k];
+            acc[r] = fma(xv, yv, acc[r]);
+            xx[r] = fma(xv, xv, xx[r]);
+          }
         }
       }
     }
     if (c < ncol) {
+      if (!inner)
 #pragma unroll
-      for (int r = 0; r < WR; ++r)
-        gblk[r * WIDE_COLS + c] =
-            inner ? kf_inner(G.S, acc[r]) : kf_sq(G.S, xx[r] + yy - 2.0 * acc[r]);
+        for (int r = 0; r < RPT; ++r) acc[r] = xx[r] + yy - 2.0 * acc[r];
+      if (G.S.kind == SK_LINEAR) {  // inline: no call per output
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) gblk[(r0 + r) * WIDE_COLS + c] = G.S.scale * acc[r];
+      } else {
+        kf_many(G.S, inner, acc, gblk + r0 * WIDE_COLS + c);
+      }
     }
   }
   __syncthreads();
