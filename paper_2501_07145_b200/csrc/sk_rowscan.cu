@@ -28,14 +28,23 @@ constexpr int CMAX = 16;           // columns per thread: T2 <= 4096 (cta_pair_l
 constexpr int VMAX = GEN_MAX_LEVELS - 1;  // scanned levels (1..M-1)
 constexpr int YSTAGE_BYTES = 96 * 1024;   // dynamic shared memory: y staging / wide blocks
 constexpr int WR = 16, KW = 16;           // wide path: point-kernel rows per block, channels per stage
-constexpr int WIDE_COLS = (YSTAGE_BYTES / 8 - WR * KW - RT * KW) / WR;  // max columns of a block
+constexpr int WIDE_COLS = (YSTAGE_BYTES / 8 - WR * KW - RT * (KW + 1)) / WR;  // max columns of a block
 __device__ __forceinline__ int64_t ystage_doubles() { return YSTAGE_BYTES / 8; }
 
 // The static kernel evaluations of this file are out-of-line calls: inlined
 // into every unrolled instance they made ptxas take over ten minutes.
+// y's channels ystride apart (1: a point-major row; ly: the channel-major staging)
 __device__ __noinline__ double kf_eval(const StaticF64 &S, const double *x, const double *y,
-                                       int d) {
-  return static_eval_f64(S, x, y, d);
+                                       int64_t ystride, int d) {
+  double xy = 0.0, xx = 0.0, yy = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const double yv = y[k * ystride];
+    xy = fma(x[k], yv, xy);
+    xx = fma(x[k], x[k], xx);
+    yy = fma(yv, yv, yy);
+  }
+  if (S.kind == SK_LINEAR || S.kind == SK_POLYNOMIAL) return static_from_inner(S, xy);
+  return static_from_sq(S, xx + yy - 2.0 * xy);  // static_eval_f64's formula
 }
 __device__ __noinline__ double kf_sq(const StaticF64 &S, double sq) {
   return static_from_sq(S, sq);
@@ -153,21 +162,23 @@ __device__ __noinline__ void wide_block(const Geo &G, const double *__restrict__
       for (int u = 0; u < XE; ++u)
         if (t + u * RT < WR * KW) xt[t + u * RT] = xr[u];
 #pragma unroll
-      for (int u = 0; u < YE; ++u)
-        if (t + u * RT < CPP * KW) yt[t + u * RT] = yr[u];
+      for (int u = 0; u < YE; ++u) {  // rows padded to KW + 1: conflict-free column reads
+        const int e = t + u * RT;
+        if (e < CPP * KW) yt[(e / KW) * (KW + 1) + e % KW] = yr[u];
+      }
       __syncthreads();
       if (k0 + KW < d) fetch(k0 + KW);
       if (inner) {
 #pragma unroll
         for (int k = 0; k < KW; ++k) {
-          const double yv = yt[ct * KW + k];
+          const double yv = yt[ct * (KW + 1) + k];
 #pragma unroll
           for (int r = 0; r < RPT; ++r) acc[r] = fma(xt[(r0 + r) * KW + k], yv, acc[r]);
         }
       } else {
 #pragma unroll
         for (int k = 0; k < KW; ++k) {
-          const double yv = yt[ct * KW + k];
+          const double yv = yt[ct * (KW + 1) + k];
           yy = fma(yv, yv, yy);
 #pragma unroll
           for (int r = 0; r < RPT; ++r) {
@@ -243,13 +254,20 @@ __device__ __noinline__ void cta_pair_levels_t(const Geo &G, const double *__res
   const int64_t ncol = G.difference ? T2 + 1 : T2;
   // narrow rows read every y point once per row: stage the pair's y sequence
   // in shared memory when it fits (ystage_doubles), else read it from L1/L2
+  // (channel-major: point c's channel k at [k * ly + c], so the threads of a
+  // warp read consecutive addresses — point-major put them 8 d bytes apart,
+  // all in one shared-memory bank)
   extern __shared__ double ystage[];
+  int64_t ysc = d, ysk = 1;  // strides of point / channel in ys
   if (!wide && ly * d <= ystage_doubles()) {
     __syncthreads();  // the previous pair's readers are done
-    for (int64_t e = t; e < ly * d; e += RT) ystage[e] = ys[e];
+    for (int64_t e = t; e < ly * d; e += RT) ystage[(e % d) * ly + e / d] = ys[e];
     __syncthreads();
     ys = ystage;
+    ysc = 1;
+    ysk = ly;
   }
+  auto yp = [&](int64_t c) { return ys + c * ysc; };
   auto wide_row = [&](const double *xa) {  // grow[c] = k(xa, y_c), c < ncol
     for (int64_t cb = (int64_t)warp * 4; cb < ncol; cb += NW * 4) {
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
@@ -370,7 +388,7 @@ __device__ __noinline__ void cta_pair_levels_t(const Geo &G, const double *__res
       } else {
 #pragma unroll
         for (int k = 0; k <= CC; ++k)
-          gp[k] = k <= n ? kf_eval(G.S, xs, ys + (c0 + k) * d, d) : 0.0;
+          gp[k] = k <= n ? kf_eval(G.S, xs, yp(c0 + k), ysk, d) : 0.0;
       }
     }
     for (int64_t r = 0; r < T1; ++r) {
@@ -387,7 +405,7 @@ __device__ __noinline__ void cta_pair_levels_t(const Geo &G, const double *__res
           // G(r+1, c0 + k) for k = 1..n here; k = 0 from the previous thread
 #pragma unroll
           for (int k = 1; k <= CC; ++k)
-            g[k] = k <= n ? kf_eval(G.S, xa, ys + (c0 + k) * d, d) : 0.0;
+            g[k] = k <= n ? kf_eval(G.S, xa, yp(c0 + k), ysk, d) : 0.0;
           double last = 0.0;
 #pragma unroll
           for (int k = 1; k <= CC; ++k)
@@ -396,7 +414,7 @@ __device__ __noinline__ void cta_pair_levels_t(const Geo &G, const double *__res
           if (lane == 31) smb[warp] = last;
           __syncthreads();
           if (t == 0)
-            g[0] = kf_eval(G.S, xa, ys, d);
+            g[0] = kf_eval(G.S, xa, yp(0), ysk, d);
           else
             g[0] = lane == 0 ? smb[warp - 1] : up;
         }
@@ -413,7 +431,7 @@ __device__ __noinline__ void cta_pair_levels_t(const Geo &G, const double *__res
       } else {
 #pragma unroll
         for (int k = 0; k < CC; ++k)
-          a[k] = k < n ? kf_eval(G.S, xs + r * d, ys + (c0 + k) * d, d) : 0.0;
+          a[k] = k < n ? kf_eval(G.S, xs + r * d, yp(c0 + k), ysk, d) : 0.0;
       }
       dp_row(a);
     }
