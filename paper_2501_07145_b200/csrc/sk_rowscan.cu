@@ -324,21 +324,34 @@ __device__ __noinline__ void cta_pair_levels_t(const Geo &G, const double *__res
           }
         }
       }
-    } else {  // long rows: runtime loops (the column state is in the scratch slice anyway)
+    } else {
+      // long rows (column state in the scratch slice): level-outer order, so
+      // each level's CC accumulators are loaded and stored as one batch of
+      // independent accesses (cell-outer order chained (M-1) CC dependent
+      // global round trips per row)
+      double R[CC];
+#pragma unroll
+      for (int k = 0; k < CC; ++k) {
+        R[k] = k < n ? a[k] : 0.0;  // R_1
+        lsum[0] += R[k];
+      }
 #pragma unroll 1
-      for (int k = 0; k < n; ++k) {
-        double Rprev = a[k];
-        lsum[0] += Rprev;
-#pragma unroll 1
-        for (int m = 1; m < M; ++m) {
-          const double R = a[k] * pre[m - 1];
-          lsum[m] += R;
-          double &acc = CA(m - 1, k);
-          const double old = acc;
-          pre[m - 1] += old;
-          acc = old + Rprev;
-          Rprev = R;
+      for (int m = 1; m < M; ++m) {
+        double cav[CC];
+#pragma unroll
+        for (int k = 0; k < CC; ++k) cav[k] = k < n ? CA(m - 1, k) : 0.0;
+        double p = pre[m - 1];
+#pragma unroll
+        for (int k = 0; k < CC; ++k) {
+          const double Rn = a[k] * p;  // R_{m+1}, S_m = the prefix left of column k
+          lsum[m] += k < n ? Rn : 0.0;
+          p += cav[k];
+          cav[k] += R[k];
+          R[k] = Rn;
         }
+#pragma unroll
+        for (int k = 0; k < CC; ++k)
+          if (k < n) CA(m - 1, k) = cav[k];
       }
     }
   };
