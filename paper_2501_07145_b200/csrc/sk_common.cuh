@@ -148,7 +148,7 @@ constexpr double CERT_NOISE = 1e-5;
 constexpr double CERT_NOISE_RAW = 1e-4;
 constexpr double CERT_TAU_NORM = 0.05;
 constexpr double CERT_TAU_RAW = 0.01;
-constexpr double CERT_TAU_RAW_LINEAR = 0.1;
+constexpr double CERT_TAU_RAW_LINEAR = 0.15;
 
 // ---------------------------------------------------------------------------
 // Level-sum epilogue: kernels.py:586-600 (+ _normalize_levelwise 510-516,

@@ -482,6 +482,182 @@ __device__ __noinline__ void cta_pair_levels(const Geo &G, const double *__restr
 #undef SK_RS
 }
 
+// --- wide short pairs (d >= 32, L <= 128): block DGEMM + one-warp DP --------
+// The redo of the GEMM-fed path's flagged entries (c4: 3.9% of a 4096^2 Gram)
+// is float64 GEMM work: 2.1 M FMAs per pair at d = 128. One CTA forms the
+// pair's whole increment (linear) or point-kernel matrix in shared memory
+// with a register-blocked float64 product (8 x 8 outputs per thread, 16
+// channels per stage), then warp 0 runs the recursion on it (lanes own 4
+// columns, one warp-level scan per level and row, no block barriers).
+constexpr int WP = 128;          // max points (rows / columns) of a wide short pair
+constexpr int WPS = WP + 1;      // padded row stride of the matrix in shared memory
+constexpr int WK = 16;           // channels per stage
+constexpr int WKS = WK + 1;
+constexpr size_t WIDE_SMEM = (size_t)(WP * WPS + 2 * WP * WKS + 2 * WP) * 8;
+
+bool wide_short(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
+  const int p = std::max(1, std::min(c.order, std::max(c.n_levels, 1)));
+  return p == 1 && d >= 32 && lx <= WP && ly <= WP && c.n_levels <= GEN_MAX_LEVELS;
+}
+
+// Level values of one pair into lv_out (written by thread 0, visible after return).
+template <int MB>
+__device__ __noinline__ void wide_pair_levels(const Geo &G, const double *__restrict__ xs,
+                                              int64_t lx, const double *__restrict__ ys,
+                                              int64_t ly, double *smem, double *lv_out) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, d = (int)G.d, M = G.M;
+  const bool inner = G.S.kind == SK_LINEAR || G.S.kind == SK_POLYNOMIAL;
+  // linear with differences: the increments' product is A itself (kernels.py:281 is
+  // bilinear); otherwise the point kernel, double-differenced when read
+  const bool incr = G.S.kind == SK_LINEAR && G.difference;
+  const int T1 = (int)(G.difference ? lx - 1 : lx), T2 = (int)(G.difference ? ly - 1 : ly);
+  if (M == 0 || T1 <= 0 || T2 <= 0) {
+    if (t == 0) {
+      lv_out[0] = 1.0;
+      for (int m = 1; m <= M; ++m) lv_out[m] = 0.0;
+    }
+    __syncthreads();
+    return;
+  }
+  const int R = incr ? T1 : (int)lx, C = incr ? T2 : (int)ly;  // matrix formed
+  double *Am = smem, *xt = Am + WP * WPS, *yt = xt + WP * WKS, *xn = yt + WP * WKS, *yn = xn + WP;
+  const int ty = t >> 4, tx = t & 15;
+  double acc[8][8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) acc[u][v] = 0.0;
+  double nrm = 0.0;  // |x_r|^2 (t < 128) or |y_c|^2 (t >= 128): stationary kinds
+  for (int k0 = 0; k0 < d; k0 += WK) {
+    __syncthreads();
+    for (int e = t; e < WP * WK; e += RT) {
+      const int r = e / WK, k = e % WK, kk = k0 + k;
+      double xv = 0.0, yv = 0.0;
+      if (kk < d) {
+        if (r < R) xv = incr ? xs[(r + 1) * d + kk] - xs[r * d + kk] : xs[r * d + kk];
+        if (r < C) yv = incr ? ys[(r + 1) * d + kk] - ys[r * d + kk] : ys[r * d + kk];
+      }
+      xt[r * WKS + k] = xv;
+      yt[r * WKS + k] = yv;
+    }
+    __syncthreads();
+    if (!inner) {
+      const double *row = t < WP ? xt + t * WKS : yt + (t - WP) * WKS;
+#pragma unroll
+      for (int k = 0; k < WK; ++k) nrm = fma(row[k], row[k], nrm);
+    }
+#pragma unroll 4
+    for (int k = 0; k < WK; ++k) {
+      double xv[8], yv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xv[u] = xt[(ty + 16 * u) * WKS + k];
+#pragma unroll
+      for (int v = 0; v < 8; ++v) yv[v] = yt[(tx + 16 * v) * WKS + k];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) acc[u][v] = fma(xv[u], yv[v], acc[u][v]);
+    }
+  }
+  if (!inner) (t < WP ? xn[t] : yn[t - WP]) = nrm;
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const int r = ty + 16 * u, c = tx + 16 * v;
+      if (r < R && c < C) {
+        const double xy = acc[u][v];
+        Am[r * WPS + c] = incr ? G.S.scale * xy
+                               : (inner ? static_from_inner(G.S, xy)
+                                        : static_from_sq(G.S, xn[r] + yn[c] - 2.0 * xy));
+      }
+    }
+  __syncthreads();
+  if (warp == 0) {
+    constexpr int VB = MB - 1;
+    double ca[VB > 0 ? VB : 1][4], lsum[MB];
+#pragma unroll
+    for (int m = 0; m < VB; ++m)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ca[m][k] = 0.0;
+#pragma unroll
+    for (int m = 0; m < MB; ++m) lsum[m] = 0.0;
+    const int c0 = 4 * lane;
+    for (int i = 0; i < T1; ++i) {
+      double a[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = c0 + k;
+        if (c >= T2) {
+          a[k] = 0.0;
+        } else if (incr || !G.difference) {
+          a[k] = Am[i * WPS + c];
+        } else {  // kernels.py:281: G[1:,1:] - G[:-1,1:] - G[1:,:-1] + G[:-1,:-1]
+          a[k] = Am[(i + 1) * WPS + c + 1] - Am[i * WPS + c + 1] - Am[(i + 1) * WPS + c] +
+                 Am[i * WPS + c];
+        }
+      }
+      // exclusive prefix over columns of every level's accumulators (old values)
+      double pre[VB > 0 ? VB : 1];
+#pragma unroll
+      for (int m = 0; m < VB; ++m) pre[m] = ca[m][0] + ca[m][1] + ca[m][2] + ca[m][3];
+#pragma unroll
+      for (int m = 0; m < VB; ++m) {
+        if (m + 1 < M) {
+          double inc = pre[m];
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const double u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+          }
+          pre[m] = inc - pre[m];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        double Rprev = a[k];
+        lsum[0] += Rprev;
+#pragma unroll
+        for (int m = 1; m < MB; ++m) {
+          if (m < M) {
+            const double Rn = a[k] * pre[m - 1];
+            lsum[m] += Rn;
+            pre[m - 1] += ca[m - 1][k];
+            ca[m - 1][k] += Rprev;
+            Rprev = Rn;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MB; ++m) {
+      double v = lsum[m];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      lsum[m] = v;
+    }
+    if (lane == 0) {
+      lv_out[0] = 1.0;
+#pragma unroll
+      for (int m = 0; m < MB; ++m)
+        if (m < M) lv_out[m + 1] = lsum[m];
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __noinline__ void wide_levels(const Geo &G, const double *xs, int64_t lx,
+                                         const double *ys, int64_t ly, double *smem,
+                                         double *lv_out) {
+  if (G.M <= 4)
+    wide_pair_levels<4>(G, xs, lx, ys, ly, smem, lv_out);
+  else if (G.M <= 8)
+    wide_pair_levels<8>(G, xs, lx, ys, ly, smem, lv_out);
+  else
+    wide_pair_levels<16>(G, xs, lx, ys, ly, smem, lv_out);
+}
+
 // --- the order-1 float64 Gram / self levels ---------------------------------
 struct GramArgs {
   Geo G;
@@ -497,7 +673,8 @@ struct GramArgs {
   int64_t slot;  // doubles of scratch per CTA
 };
 
-__global__ void __launch_bounds__(RT, 2) gram_kernel(GramArgs A) {
+template <bool WIDE>
+__global__ void __launch_bounds__(RT, WIDE ? 1 : 2) gram_kernel(GramArgs A) {
   __shared__ double sm[NW * (VMAX + 1) + NW + 2 * (GEN_MAX_LEVELS + 1)];
   double *lv = sm + NW * (VMAX + 1) + NW;
   const Geo &G = A.G;
@@ -514,7 +691,12 @@ __global__ void __launch_bounds__(RT, 2) gram_kernel(GramArgs A) {
     }
     const double *xs = G.X + i * G.lx * G.d;
     const double *ys = (A.mode == 2 ? G.X : G.Y) + j * (A.mode == 2 ? G.lx : G.ly) * G.d;
-    cta_pair_levels(G, xs, G.lx, ys, A.mode == 2 ? G.lx : G.ly, colacc, sm, lv);
+    if constexpr (WIDE) {
+      extern __shared__ double wsm[];
+      wide_levels(G, xs, G.lx, ys, A.mode == 2 ? G.lx : G.ly, wsm, lv);
+    } else {
+      cta_pair_levels(G, xs, G.lx, ys, A.mode == 2 ? G.lx : G.ly, colacc, sm, lv);
+    }
     if (threadIdx.x == 0) {
       const int M = G.M;
       if (A.mode == 2) {
@@ -683,7 +865,8 @@ __global__ void __launch_bounds__(RT) cert_scan_kernel(CertArgs A, const double 
 
 // Pass 2: CTAs stride over the entries RT at a time and recompute every NaN
 // entry in float64, one pair (plus both self levels when normalised) per CTA.
-__global__ void __launch_bounds__(RT, 2) cert_redo_kernel(CertArgs A) {
+template <bool WIDE>
+__global__ void __launch_bounds__(RT, WIDE ? 1 : 2) cert_redo_kernel(CertArgs A) {
   __shared__ double sm[NW * (VMAX + 1) + NW + 3 * (GEN_MAX_LEVELS + 1)];
   __shared__ int64_t list[RT];
   __shared__ int cnt;
@@ -710,10 +893,19 @@ __global__ void __launch_bounds__(RT, 2) cert_redo_kernel(CertArgs A) {
       const int64_t r = ee / G.ny, j = ee % G.ny, i = A.row_begin + r;
       const int64_t row = sym ? i : r;
       const double *xs = G.X + i * G.lx * G.d, *ys = G.Y + j * G.ly * G.d;
-      cta_pair_levels(G, xs, G.lx, ys, G.ly, colacc, sm, lv);
-      if (A.norm != SK_NORM_NONE) {
-        cta_pair_levels(G, xs, G.lx, xs, G.lx, colacc, sm, dx);
-        cta_pair_levels(G, ys, G.ly, ys, G.ly, colacc, sm, dy);
+      if constexpr (WIDE) {
+        extern __shared__ double wsm[];
+        wide_levels(G, xs, G.lx, ys, G.ly, wsm, lv);
+        if (A.norm != SK_NORM_NONE) {
+          wide_levels(G, xs, G.lx, xs, G.lx, wsm, dx);
+          wide_levels(G, ys, G.ly, ys, G.ly, wsm, dy);
+        }
+      } else {
+        cta_pair_levels(G, xs, G.lx, ys, G.ly, colacc, sm, lv);
+        if (A.norm != SK_NORM_NONE) {
+          cta_pair_levels(G, xs, G.lx, xs, G.lx, colacc, sm, dx);
+          cta_pair_levels(G, ys, G.ly, ys, G.ly, colacc, sm, dy);
+        }
       }
       if (threadIdx.x == 0) {
         const double v =
@@ -831,12 +1023,20 @@ int rowscan_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64
   const int64_t npairs = mode == 2 ? nx : A.rows * ny;
   if (npairs <= 0) return SK_OK;
   A.slot = slot_doubles(lx, mode == 2 ? lx : ly, c);
+  if (wide_short(lx, mode == 2 ? lx : ly, d, c)) {  // block DGEMM + one-warp DP per pair
+    const int64_t grid = std::min<int64_t>(npairs, (int64_t)sm_count());
+    SK_CHECK_CUDA(cudaFuncSetAttribute(gram_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WIDE_SMEM));
+    gram_kernel<true><<<(unsigned)grid, RT, WIDE_SMEM, st>>>(A);
+    SK_CHECK_LAUNCH();
+    return SK_OK;
+  }
   const int64_t grid = grid_for(npairs, A.slot);
   if (!ws || ws_bytes < (size_t)(grid * A.slot * 8))
     return fail(SK_ERR_WORKSPACE, "workspace too small for the float64 row-scan kernel");
   A.scratch = (double *)ws;
-  SK_CHECK_CUDA(cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, YSTAGE_BYTES));
-  gram_kernel<<<(unsigned)grid, RT, YSTAGE_BYTES, st>>>(A);
+  SK_CHECK_CUDA(cudaFuncSetAttribute(gram_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, YSTAGE_BYTES));
+  gram_kernel<false><<<(unsigned)grid, RT, YSTAGE_BYTES, st>>>(A);
   SK_CHECK_LAUNCH();
   return SK_OK;
 }
@@ -893,10 +1093,18 @@ int cert_fixup(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t
     SK_CHECK_LAUNCH();
   }
   A.slot = slot_doubles(lx, ly, c);
-  const int64_t grid = std::min<int64_t>(grid_for(1ll << 40, A.slot), (total + RT - 1) / RT);
   A.scratch = (double *)ws;
-  SK_CHECK_CUDA(cudaFuncSetAttribute(cert_redo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, YSTAGE_BYTES));
-  cert_redo_kernel<<<(unsigned)grid, RT, YSTAGE_BYTES, st>>>(A);
+  if (wide_short(lx, ly, d, c)) {  // block DGEMM + one-warp DP, one CTA per SM
+    const int64_t grid = std::min<int64_t>(sm_count(), (total + RT - 1) / RT);
+    SK_CHECK_CUDA(cudaFuncSetAttribute(cert_redo_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WIDE_SMEM));
+    cert_redo_kernel<true><<<(unsigned)grid, RT, WIDE_SMEM, st>>>(A);
+  } else {
+    const int64_t grid = std::min<int64_t>(grid_for(1ll << 40, A.slot), (total + RT - 1) / RT);
+    SK_CHECK_CUDA(cudaFuncSetAttribute(cert_redo_kernel<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, YSTAGE_BYTES));
+    cert_redo_kernel<false><<<(unsigned)grid, RT, YSTAGE_BYTES, st>>>(A);
+  }
   SK_CHECK_LAUNCH();
   return SK_OK;
 }

@@ -36,4 +36,14 @@ tol = 1e-4 if norm == "none" else 1e-5
 out = {"config": name, "entries": int(err.size), "max_rel_err": float(err.max()),
        "median_rel_err": float(np.median(err)), "p999_rel_err": float(np.percentile(err, 99.9)),
        "above_tol": int((err > tol).sum()), "tol": tol}
+bad = np.argwhere(err > tol)
+if len(bad):  # the worst offenders: their FP32 cancellation ratio |K| / sum_m |k_m|
+    from paper_2501_07145_b200 import _native
+    from paper_2501_07145_b200.kernels import gram_block
+    Xs, Ys = X[torch.from_numpy(ri[bad[:4, 0]]).cuda()], Y[torch.from_numpy(ci[bad[:4, 1]]).cuda()]
+    K0, lv = gram_block(Xs, Ys, cfg, want_levels=True, flags=_native.SK_FLAG_NO_FIXUP)
+    lvc = lv.cpu().numpy()
+    out["offenders"] = [{"err": float(err[a, b]), "K": float(R[a, b]),
+                         "ratio": float(abs(lvc[q, q].sum()) / np.abs(lvc[q, q]).sum())}
+                        for q, (a, b) in enumerate(bad[:4])]
 print(json.dumps(out))
