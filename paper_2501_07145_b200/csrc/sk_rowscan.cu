@@ -483,44 +483,45 @@ __device__ __noinline__ void cta_pair_levels(const Geo &G, const double *__restr
 }
 
 // --- wide short pairs (d >= 32, L <= 128): block DGEMM + one-warp DP --------
-// The redo of the GEMM-fed path's flagged entries (c4: 3.9% of a 4096^2 Gram)
+// The redo of the GEMM-fed path's flagged entries (c4: ~6% of a 4096^2 Gram)
 // is float64 GEMM work: 2.1 M FMAs per pair at d = 128. One CTA forms the
-// pair's whole increment (linear) or point-kernel matrix in shared memory
-// with a register-blocked float64 product (8 x 8 outputs per thread, 16
-// channels per stage), then warp 0 runs the recursion on it (lanes own 4
-// columns, one warp-level scan per level and row, no block barriers).
+// pair's whole point-kernel matrix in shared memory with a register-blocked
+// float64 product (8 x 8 outputs per thread, 16 channels per stage, the raw
+// points of the next stage in flight by cp.async while the current one is
+// multiplied), then warp 0 runs the recursion on it, double-differencing on
+// read (kernels.py:281; lanes own 4 columns, one warp-level scan per level and
+// row, no block barriers).
 constexpr int WP = 128;          // max points (rows / columns) of a wide short pair
 constexpr int WPS = WP + 1;      // padded row stride of the matrix in shared memory
 constexpr int WK = 16;           // channels per stage
 constexpr int WKS = WK + 1;
-constexpr size_t WIDE_SMEM = (size_t)(WP * WPS + 2 * WP * WKS + 2 * WP) * 8;
+constexpr int WSTAGE = 2 * WP * WKS;  // one stage buffer: x rows then y rows
+constexpr size_t WIDE_SMEM = (size_t)(WP * WPS + 2 * WSTAGE + 2 * WP) * 8;
+
+__device__ __forceinline__ void cp_async8(double *smem_dst, const double *gmem_src) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem_src));
+}
+__device__ __forceinline__ void cp_async_commit8() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait8() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 bool wide_short(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   const int p = std::max(1, std::min(c.order, std::max(c.n_levels, 1)));
   return p == 1 && d >= 32 && lx <= WP && ly <= WP && c.n_levels <= GEN_MAX_LEVELS;
 }
 
-// Level values of one pair into lv_out (written by thread 0, visible after return).
-template <int MB>
-__device__ __noinline__ void wide_pair_levels(const Geo &G, const double *__restrict__ xs,
-                                              int64_t lx, const double *__restrict__ ys,
-                                              int64_t ly, double *smem, double *lv_out) {
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, d = (int)G.d, M = G.M;
+// The pair's point-kernel matrix Am[r][c] = k(x_r, y_c) (r < lx, c < ly) into
+// shared memory (row stride WPS). All threads call it; Am is complete on return.
+__device__ __noinline__ void wide_point_matrix(const Geo &G, const double *__restrict__ xs,
+                                               int64_t lx, const double *__restrict__ ys,
+                                               int64_t ly, double *smem) {
+  const int t = threadIdx.x, d = (int)G.d;
   const bool inner = G.S.kind == SK_LINEAR || G.S.kind == SK_POLYNOMIAL;
-  // linear with differences: the increments' product is A itself (kernels.py:281 is
-  // bilinear); otherwise the point kernel, double-differenced when read
-  const bool incr = G.S.kind == SK_LINEAR && G.difference;
-  const int T1 = (int)(G.difference ? lx - 1 : lx), T2 = (int)(G.difference ? ly - 1 : ly);
-  if (M == 0 || T1 <= 0 || T2 <= 0) {
-    if (t == 0) {
-      lv_out[0] = 1.0;
-      for (int m = 1; m <= M; ++m) lv_out[m] = 0.0;
-    }
-    __syncthreads();
-    return;
-  }
-  const int R = incr ? T1 : (int)lx, C = incr ? T2 : (int)ly;  // matrix formed
-  double *Am = smem, *xt = Am + WP * WPS, *yt = xt + WP * WKS, *xn = yt + WP * WKS, *yn = xn + WP;
+  const int R = (int)lx, C = (int)ly;  // the point-kernel matrix formed
+  double *Am = smem, *stg = Am + WP * WPS, *xn = stg + 2 * WSTAGE, *yn = xn + WP;
   const int ty = t >> 4, tx = t & 15;
   double acc[8][8];
 #pragma unroll
@@ -528,17 +529,24 @@ __device__ __noinline__ void wide_pair_levels(const Geo &G, const double *__rest
 #pragma unroll
     for (int v = 0; v < 8; ++v) acc[u][v] = 0.0;
   double nrm = 0.0;  // |x_r|^2 (t < 128) or |y_c|^2 (t >= 128): stationary kinds
-  for (int k0 = 0; k0 < d; k0 += WK) {
-    __syncthreads();
+  const auto issue = [&](int k0, double *buf) {
     for (int e = t; e < WP * WK; e += RT) {
       const int r = e / WK, k = e % WK, kk = k0 + k;
-      double xv = 0.0, yv = 0.0;
-      if (kk < d) {
-        if (r < R) xv = incr ? xs[(r + 1) * d + kk] - xs[r * d + kk] : xs[r * d + kk];
-        if (r < C) yv = incr ? ys[(r + 1) * d + kk] - ys[r * d + kk] : ys[r * d + kk];
-      }
-      xt[r * WKS + k] = xv;
-      yt[r * WKS + k] = yv;
+      double *xd = buf + r * WKS + k, *yd = buf + WP * WKS + r * WKS + k;
+      if (kk < d && r < R) cp_async8(xd, xs + r * d + kk); else *xd = 0.0;
+      if (kk < d && r < C) cp_async8(yd, ys + r * d + kk); else *yd = 0.0;
+    }
+    cp_async_commit8();
+  };
+  __syncthreads();  // the previous pair's readers of the stage buffers are done
+  issue(0, stg);
+  for (int s = 0, k0 = 0; k0 < d; ++s, k0 += WK) {
+    const double *xt = stg + (s & 1) * WSTAGE, *yt = xt + WP * WKS;
+    if (k0 + WK < d) {
+      issue(k0 + WK, stg + ((s + 1) & 1) * WSTAGE);
+      cp_async_wait8<1>();
+    } else {
+      cp_async_wait8<0>();
     }
     __syncthreads();
     if (!inner) {
@@ -558,6 +566,7 @@ __device__ __noinline__ void wide_pair_levels(const Geo &G, const double *__rest
 #pragma unroll
         for (int v = 0; v < 8; ++v) acc[u][v] = fma(xv[u], yv[v], acc[u][v]);
     }
+    __syncthreads();  // this buffer is refilled two stages on
   }
   if (!inner) (t < WP ? xn[t] : yn[t - WP]) = nrm;
   __syncthreads();
@@ -568,82 +577,105 @@ __device__ __noinline__ void wide_pair_levels(const Geo &G, const double *__rest
       const int r = ty + 16 * u, c = tx + 16 * v;
       if (r < R && c < C) {
         const double xy = acc[u][v];
-        Am[r * WPS + c] = incr ? G.S.scale * xy
-                               : (inner ? static_from_inner(G.S, xy)
-                                        : static_from_sq(G.S, xn[r] + yn[c] - 2.0 * xy));
+        Am[r * WPS + c] = inner ? static_from_inner(G.S, xy)
+                                : static_from_sq(G.S, xn[r] + yn[c] - 2.0 * xy);
       }
     }
   __syncthreads();
-  if (warp == 0) {
-    constexpr int VB = MB - 1;
-    double ca[VB > 0 ? VB : 1][4], lsum[MB];
+}
+
+// The order-1 recursion of one pair by one warp on a matrix a(i, c) (i < T1,
+// c < T2 <= 128): lanes own 4 columns, one warp-level exclusive scan per level
+// and row (kernels.py:144-201). Lane 0 writes lv_out[0..M].
+template <int MB, class F>
+__device__ __forceinline__ void warp_levels(F a_of, int T1, int T2, int M, int lane,
+                                            double *lv_out) {
+  constexpr int VB = MB - 1;
+  double ca[VB > 0 ? VB : 1][4], lsum[MB];
 #pragma unroll
-    for (int m = 0; m < VB; ++m)
+  for (int m = 0; m < VB; ++m)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) ca[m][k] = 0.0;
+    for (int k = 0; k < 4; ++k) ca[m][k] = 0.0;
 #pragma unroll
-    for (int m = 0; m < MB; ++m) lsum[m] = 0.0;
-    const int c0 = 4 * lane;
-    for (int i = 0; i < T1; ++i) {
-      double a[4];
+  for (int m = 0; m < MB; ++m) lsum[m] = 0.0;
+  const int c0 = 4 * lane;
+  for (int i = 0; i < T1; ++i) {
+    double a[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int c = c0 + k;
-        if (c >= T2) {
-          a[k] = 0.0;
-        } else if (incr || !G.difference) {
-          a[k] = Am[i * WPS + c];
-        } else {  // kernels.py:281: G[1:,1:] - G[:-1,1:] - G[1:,:-1] + G[:-1,:-1]
-          a[k] = Am[(i + 1) * WPS + c + 1] - Am[i * WPS + c + 1] - Am[(i + 1) * WPS + c] +
-                 Am[i * WPS + c];
+    for (int k = 0; k < 4; ++k) a[k] = c0 + k < T2 ? a_of(i, c0 + k) : 0.0;
+    // exclusive prefix over columns of every level's accumulators (old values)
+    double pre[VB > 0 ? VB : 1];
+#pragma unroll
+    for (int m = 0; m < VB; ++m) pre[m] = ca[m][0] + ca[m][1] + ca[m][2] + ca[m][3];
+#pragma unroll
+    for (int m = 0; m < VB; ++m) {
+      if (m + 1 < M) {
+        double inc = pre[m];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double u = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += u;
         }
-      }
-      // exclusive prefix over columns of every level's accumulators (old values)
-      double pre[VB > 0 ? VB : 1];
-#pragma unroll
-      for (int m = 0; m < VB; ++m) pre[m] = ca[m][0] + ca[m][1] + ca[m][2] + ca[m][3];
-#pragma unroll
-      for (int m = 0; m < VB; ++m) {
-        if (m + 1 < M) {
-          double inc = pre[m];
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const double u = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += u;
-          }
-          pre[m] = inc - pre[m];
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        double Rprev = a[k];
-        lsum[0] += Rprev;
-#pragma unroll
-        for (int m = 1; m < MB; ++m) {
-          if (m < M) {
-            const double Rn = a[k] * pre[m - 1];
-            lsum[m] += Rn;
-            pre[m - 1] += ca[m - 1][k];
-            ca[m - 1][k] += Rprev;
-            Rprev = Rn;
-          }
-        }
+        pre[m] = inc - pre[m];
       }
     }
 #pragma unroll
-    for (int m = 0; m < MB; ++m) {
-      double v = lsum[m];
+    for (int k = 0; k < 4; ++k) {
+      double Rprev = a[k];
+      lsum[0] += Rprev;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      lsum[m] = v;
-    }
-    if (lane == 0) {
-      lv_out[0] = 1.0;
-#pragma unroll
-      for (int m = 0; m < MB; ++m)
-        if (m < M) lv_out[m + 1] = lsum[m];
+      for (int m = 1; m < MB; ++m) {
+        if (m < M) {
+          const double Rn = a[k] * pre[m - 1];
+          lsum[m] += Rn;
+          pre[m - 1] += ca[m - 1][k];
+          ca[m - 1][k] += Rprev;
+          Rprev = Rn;
+        }
+      }
     }
   }
+#pragma unroll
+  for (int m = 0; m < MB; ++m) {
+    double v = lsum[m];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    lsum[m] = v;
+  }
+  if (lane == 0) {
+    lv_out[0] = 1.0;
+#pragma unroll
+    for (int m = 0; m < MB; ++m)
+      if (m < M) lv_out[m + 1] = lsum[m];
+  }
+}
+
+// Level values of one pair into lv_out (written by thread 0, visible after return).
+template <int MB>
+__device__ __noinline__ void wide_pair_levels(const Geo &G, const double *__restrict__ xs,
+                                              int64_t lx, const double *__restrict__ ys,
+                                              int64_t ly, double *smem, double *lv_out) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, M = G.M;
+  const int T1 = (int)(G.difference ? lx - 1 : lx), T2 = (int)(G.difference ? ly - 1 : ly);
+  if (M == 0 || T1 <= 0 || T2 <= 0) {
+    if (t == 0) {
+      lv_out[0] = 1.0;
+      for (int m = 1; m <= M; ++m) lv_out[m] = 0.0;
+    }
+    __syncthreads();
+    return;
+  }
+  wide_point_matrix(G, xs, lx, ys, ly, smem);
+  const double *Am = smem;
+  const bool diff = G.difference;
+  if (warp == 0)
+    warp_levels<MB>(
+        [&](int i, int c) {
+          return diff ? Am[(i + 1) * WPS + c + 1] - Am[i * WPS + c + 1] - Am[(i + 1) * WPS + c] +
+                            Am[i * WPS + c]
+                      : Am[i * WPS + c];
+        },
+        T1, T2, M, lane, lv_out);
   __syncthreads();
 }
 
@@ -735,7 +767,17 @@ struct CertArgs {
   double *levels;
   double *scratch;
   int64_t slot;
+  // compacted list of the entries the scan flagged: work[0] = count, then the
+  // entry indices (row - row_begin) * ny + j; a count above `cap` (or no scan)
+  // makes the redo find its entries by scanning K instead
+  unsigned long long *work;
+  int64_t cap;
 };
+
+__device__ __forceinline__ void flag_entry(const CertArgs &A, int64_t e) {
+  const unsigned long long q = atomicAdd(A.work, 1ull);
+  if ((int64_t)q < A.cap) A.work[1 + q] = (unsigned long long)e;
+}
 
 // Pass 1: the exact-level-1 check. The four corner point-kernel values of
 // every entry are a small GEMM-shaped contraction over the channels, so CTAs
@@ -821,6 +863,7 @@ __global__ void __launch_bounds__(RT) cert_scan_kernel(CertArgs A, const double 
       if (!(fabs(v) >= lim) || isinf(v)) {
         *kp = __longlong_as_double(0x7ff8000000000000ll);
         if (sym) A.K[j * A.ldk + i] = *kp;
+        flag_entry(A, (r0 + r) * G.ny + j);
         continue;
       }
       if (!A.l1check) continue;
@@ -855,6 +898,7 @@ __global__ void __launch_bounds__(RT) cert_scan_kernel(CertArgs A, const double 
                             : v + corr;
       *kp = nv;
       if (sym) A.K[j * A.ldk + i] = nv;
+      if (isnan(nv)) flag_entry(A, (r0 + r) * G.ny + j);
       if (A.levels && !isnan(nv)) {
         A.levels[(row * A.ldk + j) * (M + 1) + 1] = k1e;
         if (sym) A.levels[(j * A.ldk + i) * (M + 1) + 1] = k1e;
@@ -863,8 +907,139 @@ __global__ void __launch_bounds__(RT) cert_scan_kernel(CertArgs A, const double 
   }
 }
 
-// Pass 2: CTAs stride over the entries RT at a time and recompute every NaN
-// entry in float64, one pair (plus both self levels when normalised) per CTA.
+// Pass 2: every flagged entry recomputed in float64, one pair (plus both self
+// levels when normalised) per CTA. The scan's compacted list is dealt out
+// round-robin (every item costs the same, and flagged entries cluster in rows,
+// so striding over K itself left most CTAs idle); without a list the CTAs
+// stride over the entries RT at a time and collect the NaN ones.
+template <bool WIDE>
+__device__ void redo_entry(const CertArgs &A, int64_t ee, double *colacc, double *sm,
+                           double *lv, double *dx, double *dy) {
+  const Geo &G = A.G;
+  const int M = G.M;
+  const bool sym = A.symmetric;
+  const int64_t r = ee / G.ny, j = ee % G.ny, i = A.row_begin + r;
+  const int64_t row = sym ? i : r;
+  const double *xs = G.X + i * G.lx * G.d, *ys = G.Y + j * G.ly * G.d;
+  if constexpr (WIDE) {
+    extern __shared__ double wsm[];
+    wide_levels(G, xs, G.lx, ys, G.ly, wsm, lv);
+    if (A.norm != SK_NORM_NONE) {
+      wide_levels(G, xs, G.lx, xs, G.lx, wsm, dx);
+      wide_levels(G, ys, G.ly, ys, G.ly, wsm, dy);
+    }
+  } else {
+    cta_pair_levels(G, xs, G.lx, ys, G.ly, colacc, sm, lv);
+    if (A.norm != SK_NORM_NONE) {
+      cta_pair_levels(G, xs, G.lx, xs, G.lx, colacc, sm, dx);
+      cta_pair_levels(G, ys, G.ly, ys, G.ly, colacc, sm, dy);
+    }
+  }
+  if (threadIdx.x == 0) {
+    const double v = finish_entry(lv, M, A.norm, A.norm != SK_NORM_NONE ? dx : nullptr,
+                                  A.norm != SK_NORM_NONE ? dy : nullptr);
+    A.K[row * A.ldk + j] = v;
+    if (sym && j != i) A.K[j * A.ldk + i] = v;
+    if (A.levels) {
+      for (int m = 0; m <= M; ++m) A.levels[(row * A.ldk + j) * (M + 1) + m] = lv[m];
+      if (sym && j != i)
+        for (int m = 0; m <= M; ++m) A.levels[(j * A.ldk + i) * (M + 1) + m] = lv[m];
+    }
+  }
+  __syncthreads();
+}
+
+// Wide short pairs in batches: the CTA forms WB pairs' matrices one after the
+// other (the block DGEMM above), each double-differenced into its slot of the
+// CTA's global ring (L2-resident, WP x WP doubles), then WB warps run the
+// recursions concurrently — one warp's recursion is a ~100 us latency chain,
+// which a lone warp left the other seven waiting on.
+constexpr int WB = 8;
+constexpr int64_t WSLOT = (int64_t)WP * WP;
+
+// All threads: the matrix of one pair (T1 x T2 increments' kernel values, row
+// stride WP, zero beyond T2) into `out`.
+__device__ __noinline__ void wide_stage_pair(const Geo &G, const double *xs, int64_t lx,
+                                             const double *ys, int64_t ly, double *smem,
+                                             double *out) {
+  const int T1 = (int)(G.difference ? lx - 1 : lx), T2 = (int)(G.difference ? ly - 1 : ly);
+  if (G.M == 0 || T1 <= 0 || T2 <= 0) return;
+  wide_point_matrix(G, xs, lx, ys, ly, smem);
+  const double *Am = smem;
+  const bool diff = G.difference;
+  for (int e = threadIdx.x; e < T1 * WP; e += RT) {
+    const int i = e / WP, c = e % WP;
+    double v = 0.0;
+    if (c < T2)
+      v = diff ? Am[(i + 1) * WPS + c + 1] - Am[i * WPS + c + 1] - Am[(i + 1) * WPS + c] +
+                     Am[i * WPS + c]
+               : Am[i * WPS + c];
+    out[e] = v;
+  }
+  __syncthreads();  // Am is the next pair's
+}
+
+// The scan's listed entries (n of them): P = 1 pair per entry, or 3 (the pair
+// and both self pairs) when normalised.
+template <int MB>
+__device__ void redo_wide_batched(const CertArgs &A, int64_t n, double *slots, double *smem,
+                                  double (*lvw)[GEN_MAX_LEVELS + 1]) {
+  const Geo &G = A.G;
+  const int M = G.M, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool sym = A.symmetric, norm = A.norm != SK_NORM_NONE;
+  const int P = norm ? 3 : 1, EB = WB / P;
+  const auto pair_of = [&](int64_t ee, int role, const double *&p1, int64_t &l1,
+                           const double *&p2, int64_t &l2) {
+    const int64_t r = ee / G.ny, j = ee % G.ny, i = A.row_begin + r;
+    const double *xs = G.X + i * G.lx * G.d, *ys = G.Y + j * G.ly * G.d;
+    p1 = role == 2 ? ys : xs;
+    l1 = role == 2 ? G.ly : G.lx;
+    p2 = role == 1 ? xs : ys;
+    l2 = role == 1 ? G.lx : G.ly;
+  };
+  for (int64_t base = (int64_t)blockIdx.x * EB; base < n; base += (int64_t)gridDim.x * EB) {
+    const int nb = (int)(n - base < EB ? n - base : EB);
+    for (int b = 0; b < nb * P; ++b) {
+      const double *p1, *p2;
+      int64_t l1, l2;
+      pair_of((int64_t)A.work[1 + base + b / P], b % P, p1, l1, p2, l2);
+      wide_stage_pair(G, p1, l1, p2, l2, smem, slots + b * WSLOT);
+    }
+    if (warp < nb * P) {
+      const double *p1, *p2;
+      int64_t l1, l2;
+      pair_of((int64_t)A.work[1 + base + warp / P], warp % P, p1, l1, p2, l2);
+      const int T1 = (int)(G.difference ? l1 - 1 : l1), T2 = (int)(G.difference ? l2 - 1 : l2);
+      const double *Ag = slots + warp * WSLOT;
+      if (M == 0 || T1 <= 0 || T2 <= 0) {
+        if (lane == 0) {
+          lvw[warp][0] = 1.0;
+          for (int m = 1; m <= M; ++m) lvw[warp][m] = 0.0;
+        }
+      } else {
+        warp_levels<MB>([&](int i, int c) { return Ag[i * WP + c]; }, T1, T2, M, lane, lvw[warp]);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < nb) {
+      const int64_t ee = (int64_t)A.work[1 + base + threadIdx.x];
+      const int64_t r = ee / G.ny, j = ee % G.ny, i = A.row_begin + r;
+      const int64_t row = sym ? i : r;
+      const double *lv = lvw[threadIdx.x * P];
+      const double v = finish_entry(lv, M, A.norm, norm ? lvw[threadIdx.x * P + 1] : nullptr,
+                                    norm ? lvw[threadIdx.x * P + 2] : nullptr);
+      A.K[row * A.ldk + j] = v;
+      if (sym && j != i) A.K[j * A.ldk + i] = v;
+      if (A.levels) {
+        for (int m = 0; m <= M; ++m) A.levels[(row * A.ldk + j) * (M + 1) + m] = lv[m];
+        if (sym && j != i)
+          for (int m = 0; m <= M; ++m) A.levels[(j * A.ldk + i) * (M + 1) + m] = lv[m];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <bool WIDE>
 __global__ void __launch_bounds__(RT, WIDE ? 1 : 2) cert_redo_kernel(CertArgs A) {
   __shared__ double sm[NW * (VMAX + 1) + NW + 3 * (GEN_MAX_LEVELS + 1)];
@@ -872,9 +1047,25 @@ __global__ void __launch_bounds__(RT, WIDE ? 1 : 2) cert_redo_kernel(CertArgs A)
   __shared__ int cnt;
   double *lv = sm + NW * (VMAX + 1) + NW, *dx = lv + GEN_MAX_LEVELS + 1, *dy = dx + GEN_MAX_LEVELS + 1;
   const Geo &G = A.G;
-  const int M = G.M;
   const bool sym = A.symmetric;
   double *colacc = A.scratch + blockIdx.x * A.slot;
+  const int64_t n = A.work ? (int64_t)*A.work : A.cap + 1;
+  if (WIDE && n <= A.cap) {
+    extern __shared__ double wsm[];
+    __shared__ double lvw[WB][GEN_MAX_LEVELS + 1];
+    if (G.M <= 4)
+      redo_wide_batched<4>(A, n, colacc, wsm, lvw);
+    else if (G.M <= 8)
+      redo_wide_batched<8>(A, n, colacc, wsm, lvw);
+    else
+      redo_wide_batched<16>(A, n, colacc, wsm, lvw);
+    return;
+  }
+  if (n <= A.cap) {
+    for (int64_t q = blockIdx.x; q < n; q += gridDim.x)
+      redo_entry<WIDE>(A, (int64_t)A.work[1 + q], colacc, sm, lv, dx, dy);
+    return;
+  }
   const int64_t total = A.rows * G.ny;
   for (int64_t e0 = (int64_t)blockIdx.x * RT; e0 < total; e0 += (int64_t)gridDim.x * RT) {
     if (threadIdx.x == 0) cnt = 0;
@@ -886,41 +1077,9 @@ __global__ void __launch_bounds__(RT, WIDE ? 1 : 2) cert_redo_kernel(CertArgs A)
       if (!(sym && j < i) && isnan(A.K[row * A.ldk + j])) list[atomicAdd(&cnt, 1)] = e;
     }
     __syncthreads();
-    const int n = cnt;
+    const int nl = cnt;
     __syncthreads();  // every thread has read cnt before it is reset
-    for (int q = 0; q < n; ++q) {
-      const int64_t ee = list[q];
-      const int64_t r = ee / G.ny, j = ee % G.ny, i = A.row_begin + r;
-      const int64_t row = sym ? i : r;
-      const double *xs = G.X + i * G.lx * G.d, *ys = G.Y + j * G.ly * G.d;
-      if constexpr (WIDE) {
-        extern __shared__ double wsm[];
-        wide_levels(G, xs, G.lx, ys, G.ly, wsm, lv);
-        if (A.norm != SK_NORM_NONE) {
-          wide_levels(G, xs, G.lx, xs, G.lx, wsm, dx);
-          wide_levels(G, ys, G.ly, ys, G.ly, wsm, dy);
-        }
-      } else {
-        cta_pair_levels(G, xs, G.lx, ys, G.ly, colacc, sm, lv);
-        if (A.norm != SK_NORM_NONE) {
-          cta_pair_levels(G, xs, G.lx, xs, G.lx, colacc, sm, dx);
-          cta_pair_levels(G, ys, G.ly, ys, G.ly, colacc, sm, dy);
-        }
-      }
-      if (threadIdx.x == 0) {
-        const double v =
-            finish_entry(lv, M, A.norm, A.norm != SK_NORM_NONE ? dx : nullptr,
-                         A.norm != SK_NORM_NONE ? dy : nullptr);
-        A.K[row * A.ldk + j] = v;
-        if (sym && j != i) A.K[j * A.ldk + i] = v;
-        if (A.levels) {
-          for (int m = 0; m <= M; ++m) A.levels[(row * A.ldk + j) * (M + 1) + m] = lv[m];
-          if (sym && j != i)
-            for (int m = 0; m <= M; ++m) A.levels[(j * A.ldk + i) * (M + 1) + m] = lv[m];
-        }
-      }
-      __syncthreads();
-    }
+    for (int q = 0; q < nl; ++q) redo_entry<WIDE>(A, list[q], colacc, sm, lv, dx, dy);
   }
 }
 
@@ -979,6 +1138,12 @@ int64_t slot_doubles(int64_t lx, int64_t ly, const sk_kernel_config &c) {
   // the row buffer of the wide (d >= 32) point-kernel evaluation, then the
   // column accumulators of the long-row (more than 2 columns per thread) variant
   return L + 2 + std::max(c.n_levels - 1, 1) * T;
+}
+
+// the certification redo's per-CTA slot: wide short pairs stage WB matrices
+int64_t redo_slot_doubles(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
+  const int64_t slot = slot_doubles(lx, ly, c);
+  return wide_short(lx, ly, d, c) ? std::max(slot, WB * WSLOT) : slot;
 }
 
 int64_t grid_for(int64_t work, int64_t slot) {
@@ -1041,13 +1206,21 @@ int rowscan_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64
   return SK_OK;
 }
 
+// the scan's compacted list: a count and up to min(nx * ny, 4 Mi) entry indices
+static int64_t work_list_cap(int64_t nx, int64_t ny) {
+  return std::max<int64_t>(1, std::min<int64_t>(nx * ny, 1ll << 22));
+}
+static size_t work_list_bytes(int64_t nx, int64_t ny) {
+  return ((size_t)(work_list_cap(nx, ny) + 1) * 8 + 255) & ~(size_t)255;
+}
+
 size_t cert_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int64_t d,
                             const sk_kernel_config &c) {
   using namespace rowscan;
-  const int64_t slot = slot_doubles(lx, ly, c);
+  const int64_t slot = redo_slot_doubles(lx, ly, d, c);
   const size_t redo = (size_t)grid_for(1ll << 40, slot) * slot * 8;
   const size_t corners = (size_t)(nx + ny) * 2 * d * 8;  // scan pass, before the redo
-  return std::max(redo, corners);
+  return ((std::max(redo, corners) + 255) & ~(size_t)255) + work_list_bytes(nx, ny);
 }
 
 int cert_fixup(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny, int64_t ly,
@@ -1073,6 +1246,18 @@ int cert_fixup(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t
   if (!ws || ws_bytes < cert_workspace_bytes(nx, lx, ny, ly, d, c))
     return fail(SK_ERR_WORKSPACE, "workspace too small for the certification fix-up");
   A.l1check = c.difference && c.n_levels >= 1;
+  {
+    // the list lives after the scan / redo scratch
+    const int64_t slot = redo_slot_doubles(lx, ly, d, c);
+    const size_t redo = (size_t)grid_for(1ll << 40, slot) * slot * 8;
+    const size_t corners = (size_t)(nx + ny) * 2 * d * 8;
+    A.work = (unsigned long long *)((char *)ws + ((std::max(redo, corners) + 255) & ~(size_t)255));
+    A.cap = work_list_cap(nx, ny);
+    if (k1buf)
+      SK_CHECK_CUDA(cudaMemsetAsync(A.work, 0, 8, st));
+    else
+      A.work = nullptr;  // no scan: the redo finds the NaN entries itself
+  }
   if (k1buf) {
     // transposed corner points of both roles (scan pass only; the redo reuses the space)
     double *Xc = (double *)ws, *Yc = Xc + nx * 2 * d;
@@ -1092,7 +1277,7 @@ int cert_fixup(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t
       cert_scan_kernel<false><<<g, RT, 0, st>>>(A, Xc, Yc);
     SK_CHECK_LAUNCH();
   }
-  A.slot = slot_doubles(lx, ly, c);
+  A.slot = redo_slot_doubles(lx, ly, d, c);
   A.scratch = (double *)ws;
   if (wide_short(lx, ly, d, c)) {  // block DGEMM + one-warp DP, one CTA per SM
     const int64_t grid = std::min<int64_t>(sm_count(), (total + RT - 1) / RT);

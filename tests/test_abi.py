@@ -25,6 +25,9 @@ def test_library_loads_and_exports_header_symbols():
     assert set(names) == set(_native.EXPORTS)
     for n in names:
         assert hasattr(lib, n), n
+    c5 = _native.config_struct(KernelConfig(n_levels=8))
+    # few sequences: the certification scratch is the larger part
+    assert lib.sk_workspace_bytes(2, 256, 2, 256, 4, c5) == 256 + cert_bytes(2, 256, 2, 256, 4, 8)
     assert lib.sk_abi_version() == 2
     assert lib.sk_last_error() == b""
 
@@ -61,20 +64,29 @@ def test_fast_path_selection():
                                               order=3))
     assert lib.sk_fast_path(64, 64, 4, matp) == 0           # stationary kinds, order > 1: float64
     poly = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="polynomial")))
-    assert lib.sk_fast_path(64, 64, 4, poly) == 0           # polynomial: float64
+    assert lib.sk_fast_path(64, 64, 4, poly) == 1           # polynomial, order 1: fused
+    poly2 = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="polynomial"),
+                                               n_levels=3, order=2))
+    assert lib.sk_fast_path(64, 64, 4, poly2) == 0          # polynomial, order > 1: float64
     assert lib.sk_fast_path(300, 300, 4, c3) == 1           # two 256-column panels
     assert lib.sk_fast_path(2048, 2048, 4, _native.config_struct(KernelConfig(n_levels=8))) == 1  # c5
     assert lib.sk_fast_path(1000, 1000, 16, c3) == 2        # x ring would exceed shared memory
     assert lib.sk_fast_path(2, 256, 4, c3) == 0             # x shorter than the wavefront
 
 
-def lib_fixup_bytes(L, M, p=1):
-    # sk_generic.cu fixup_workspace_bytes: one float64 scratch slot per thread
-    # (column state (M-1)*(L-1)*p + L + 1 doubles), threads = min(148*2*128,
-    # 96 MiB / slot) rounded down to 128
-    slot = ((M - 1) * (L - 1) * p + L + 1) * 8
-    thr = min(148 * 2 * 128, (96 << 20) // slot) // 128 * 128
-    return max(thr, 128) * slot
+def _a256(b):
+    return (b + 255) // 256 * 256
+
+
+def cert_bytes(nx, lx, ny, ly, d, M):
+    # corner points of both roles (scan) or per-CTA float64 slots (redo: 4 CTAs
+    # per SM, row buffer + (M-1) column accumulators), then the compacted list
+    # of flagged entries (a count + up to min(nx*ny, 4 Mi) indices)
+    L = max(lx, ly)
+    slot = L + 2 + (M - 1) * (L - 1)
+    redo = min(148 * 4, (256 << 20) // (slot * 8)) * slot * 8
+    corners = (nx + ny) * 2 * d * 8
+    return _a256(max(redo, corners)) + _a256((min(nx * ny, 1 << 22) + 1) * 8)
 
 
 def test_workspace_sizes():
@@ -82,11 +94,12 @@ def test_workspace_sizes():
     c3 = _native.config_struct(KernelConfig(n_levels=5, normalization="levelwise"))
     n, L, d = 8192, 256, 16
     ws = lib.sk_workspace_bytes(n, L, n, L, d, c3)
-    # the certification's FP32 level-1 buffer (n x n floats), then the larger of
-    # the packed roles (x row pairs of 2*16+4 floats, y points of 16+4 floats, the
-    # midrange codes of the centring: 2d u64, 256-byte aligned) and the fix-up scratch
+    # the certification's per-entry (FP32 level 1, sum |k_m|) float pair, then the
+    # larger of the packed roles (x row pairs of 2*16+4 floats, y points of 16+4
+    # floats, the midrange codes of the centring: 2d u64, 256-byte aligned) and
+    # the certification scratch (sk_rowscan.cu cert_workspace_bytes)
     roles = n * (L // 2) * 36 * 4 + n * L * 20 * 4 + 256
-    assert ws == n * n * 4 + max(roles, lib_fixup_bytes(L, 5))
+    assert ws == n * n * 8 + max(roles, cert_bytes(n, L, n, L, d, 5))
     assert lib.sk_abi_version() == 2
     f64 = _native.config_struct(KernelConfig(n_levels=3, order=2), "fp64")
     assert lib.sk_workspace_bytes(4, 6, 5, 7, 2, f64) > 0

@@ -1,7 +1,4 @@
 set -x
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
-timeout 300 python tools/devtime.py c5 512 fp32 2 nofix 2>&1 | tail -1
-timeout 300 python tools/devtime.py c5 512 fp32 2 2>&1 | tail -1
-timeout 300 python tools/devtime.py c4 4096 fp32 2 2>&1 | tail -1
-timeout 300 python tools/diag_fp64_pair.py c3 2>&1 | tail -3
-timeout 300 python tools/diag_fp64_pair.py c5 2>&1 | tail -3
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q -x -k "polynomial or random_config" 2>&1 | tail -15
+timeout 300 python tools/diag_flags.py 2>&1 | tail -5
