@@ -575,12 +575,19 @@ __device__ __noinline__ void wide_point_matrix(const Geo &G, const double *__res
 #pragma unroll
     for (int v = 0; v < 8; ++v) {
       const int r = ty + 16 * u, c = tx + 16 * v;
-      if (r < R && c < C) {
-        const double xy = acc[u][v];
-        Am[r * WPS + c] = inner ? static_from_inner(G.S, xy)
-                                : static_from_sq(G.S, xn[r] + yn[c] - 2.0 * xy);
-      }
+      if (r < R && c < C) Am[r * WPS + c] = inner ? acc[u][v] : xn[r] + yn[c] - 2.0 * acc[u][v];
     }
+  __syncthreads();
+  // the static kernel in a rolled loop: one copy of its code (inlined into the
+  // unrolled tile above it was 64 copies, and the instruction cache missed)
+  const StaticF64 S = G.S;
+  for (int r = t / WP; r < R; r += RT / WP) {
+    const int c = t % WP;
+    if (c < C) {
+      double &v = Am[r * WPS + c];
+      v = inner ? static_from_inner(S, v) : static_from_sq(S, v);
+    }
+  }
   __syncthreads();
 }
 
@@ -599,10 +606,22 @@ __device__ __forceinline__ void warp_levels(F a_of, int T1, int T2, int M, int l
 #pragma unroll
   for (int m = 0; m < MB; ++m) lsum[m] = 0.0;
   const int c0 = 4 * lane;
+  // rows are read two ahead: the batched redo's matrices come from L2, and
+  // the recursion is one serial chain per warp
+  double nx1[4], nx2[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    nx1[k] = c0 + k < T2 ? a_of(0, c0 + k) : 0.0;
+    nx2[k] = 1 < T1 && c0 + k < T2 ? a_of(1, c0 + k) : 0.0;
+  }
   for (int i = 0; i < T1; ++i) {
     double a[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) a[k] = c0 + k < T2 ? a_of(i, c0 + k) : 0.0;
+    for (int k = 0; k < 4; ++k) {
+      a[k] = nx1[k];
+      nx1[k] = nx2[k];
+      nx2[k] = i + 2 < T1 && c0 + k < T2 ? a_of(i + 2, c0 + k) : 0.0;
+    }
     // exclusive prefix over columns of every level's accumulators (old values)
     double pre[VB > 0 ? VB : 1];
 #pragma unroll
