@@ -67,6 +67,34 @@ def order_aware_flops_per_entry(L, d, M, p):
     return L * L * per_cell
 
 
+def geo_ops_per_cell(M, p):
+    """FP32 pipe slots per cell of the general-order recursion (p > 1): every
+    FMUL / FADD / FFMA of the generated straight-line cell (sk_geo_cells.cuh,
+    one slot each whether it is worth 1 or 2 flops), counted from the header
+    the kernel compiles. The order-aware flop model above credits 2 flops per
+    state and misses the weighted row, column and total sums the recursion
+    needs (kernels.py:179-199), about 3 p^2 slots per level."""
+    import re
+    src = open(os.path.join(ROOT, "paper_2501_07145_b200", "csrc", "sk_geo_cells.cuh")).read()
+    i = src.index(f"struct GeoCell<{M}, {p}>")
+    body = src[i:src.index("};", i)]
+    n = 0
+    for ln in body.splitlines():
+        ln = ln.strip()
+        if "fmaf(" in ln or re.search(r"\+= ", ln) or re.search(r"= av \* ", ln):
+            n += 1
+    return n
+
+
+def pipe_slot_frac(L, d, M, p, pairs, ms, sms, clk_mhz):
+    """Share of the FP32 pipe's slots (148 SMs x 127.85 / clk) the p > 1 kernel
+    fills with necessary work: the generated cell's ops plus the point stage's
+    ~d + 6 (d FMAs of the inner product, the n-terms, the exp prescale and the
+    double difference)."""
+    slots = pairs * (L - 1) ** 2 * (geo_ops_per_cell(M, p) + d + 6)
+    return slots / (ms / 1e3) / (sms * FP32_LANE_OPS * clk_mhz * 1e6)
+
+
 def tensor_roofline(nx, ny, L, d, kind, call_ms):
     """3xTF32 cell-value GEMM work of one sk_gram call against the TF32 tensor peak
     (half the MEASURED_PEAKS.json dense bf16 burst figure; B200_PROFILING's
@@ -472,6 +500,12 @@ def run_gpu(args):
                          "order_aware_frac": (pairs * order_aware_flops_per_entry(L, d, M, p)
                                               / (g_ms / 1e3) / 1e12 / peak),
                          "kernel_ms": g_ms,
+                         **({"pipe_slot_frac": pipe_slot_frac(L, d, M, p, pairs, g_ms,
+                                                              props.multi_processor_count, sm_max),
+                             "pipe_slot_note": "p > 1: FP32 instruction slots of the generated "
+                                               "recursion cell + point stage, vs the pipe's "
+                                               "slot rate (bench.py geo_ops_per_cell)"}
+                            if 1 < p and path == "fused" else {}),
                          "peak_note": f"measured FP32 pipe rate: {props.multi_processor_count} "
                                       f"SMs x {FP32_LANE_OPS} lane-ops/clk (FFMA2/FADD2, "
                                       f"profiles/r2_fp32_pipes.txt) x 2 x {sm_max:.0f} MHz "
