@@ -30,6 +30,12 @@ constexpr int YSTAGE_BYTES = 96 * 1024;   // dynamic shared memory: y staging / 
 constexpr int WR = 16, KW = 16;           // wide path: point-kernel rows per block, channels per stage
 constexpr int WIDE_COLS = (YSTAGE_BYTES / 8 - WR * KW - RT * (KW + 1)) / WR;  // max columns of a block
 __device__ __forceinline__ int64_t ystage_doubles() { return YSTAGE_BYTES / 8; }
+__device__ __forceinline__ unsigned dyn_smem_bytes() {
+  unsigned r;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+  return r;
+}
+constexpr int DYN_SMEM_MAX = 200 * 1024;  // long-row launches: staged y + column state
 
 // The static kernel evaluations of this file are out-of-line calls: inlined
 // into every unrolled instance they made ptxas take over ten minutes.
@@ -225,25 +231,21 @@ __device__ __noinline__ void cta_pair_levels_t(const Geo &G, const double *__res
   constexpr bool REG = CC <= 2;
   constexpr int VB = MB - 1;  // level bound of this instance (M <= MB)
   double ca[REG ? VB : 1][REG ? CC : 1];
-  double *cmem = colacc + T2 + 2;  // after the row buffer
+  // MEM variant: the scratch slice after the row buffer ([m][column]), or
+  // shared memory after the staged y sequence when the launch gave enough
+  // ([m][k][thread], conflict-free) — L2 round trips per level and row were
+  // the long-row kernel's bound (c5 pair: 68 ms, 67% long-scoreboard stalls)
+  double *cm_base = colacc + T2 + 2 + c0;
+  int64_t cm_sm = T2, cm_sk = 1;
   auto CA = [&](int m, int k) -> double & {
     if constexpr (REG) return ca[m][k];
-    else return cmem[(int64_t)m * T2 + c0 + k];
+    else return cm_base[m * cm_sm + k * cm_sk];
   };
-  if constexpr (REG) {
-#pragma unroll
-    for (int m = 0; m < VB; ++m)
-#pragma unroll
-      for (int k = 0; k < CC; ++k) ca[m][k] = 0.0;
-  } else {
-    for (int m = 0; m < NV; ++m)
-#pragma unroll
-      for (int k = 0; k < CC; ++k)
-        if (k < n) CA(m, k) = 0.0;
-  }
-  double lsum[MB];
+  double lsum[MB], tot[VB];
 #pragma unroll
   for (int m = 0; m < MB; ++m) lsum[m] = 0.0;
+#pragma unroll
+  for (int m = 0; m < VB; ++m) tot[m] = 0.0;
   double *smb = sm + NW * VMAX;  // warp-boundary point-kernel values
   // d >= 32: a row's point-kernel values are formed warp-cooperatively (lanes
   // over channels: coalesced reads of every y point) into a row buffer in the
@@ -266,6 +268,25 @@ __device__ __noinline__ void cta_pair_levels_t(const Geo &G, const double *__res
     ys = ystage;
     ysc = 1;
     ysk = ly;
+    if constexpr (!REG) {
+      const int64_t off = (ly * d + 1) & ~(int64_t)1;
+      if ((off + (int64_t)NV * C * RT) * 8 <= (int64_t)dyn_smem_bytes()) {
+        cm_base = ystage + off + t;
+        cm_sm = (int64_t)C * RT;
+        cm_sk = RT;
+      }
+    }
+  }
+  if constexpr (REG) {
+#pragma unroll
+    for (int m = 0; m < VB; ++m)
+#pragma unroll
+      for (int k = 0; k < CC; ++k) ca[m][k] = 0.0;
+  } else {
+    for (int m = 0; m < NV; ++m)
+#pragma unroll
+      for (int k = 0; k < CC; ++k)
+        if (k < n) CA(m, k) = 0.0;
   }
   auto yp = [&](int64_t c) { return ys + c * ysc; };
   auto wide_row = [&](const double *xa) {  // grow[c] = k(xa, y_c), c < ncol
@@ -299,10 +320,11 @@ __device__ __noinline__ void cta_pair_levels_t(const Geo &G, const double *__res
 #pragma unroll
     for (int m = 0; m < VB; ++m) {
       pre[m] = 0.0;
-      if (REG || m < NV) {
+      if constexpr (REG) {
 #pragma unroll
-        for (int k = 0; k < CC; ++k)
-          if (REG || k < n) pre[m] += CA(m, k);
+        for (int k = 0; k < CC; ++k) pre[m] += CA(m, k);
+      } else {
+        pre[m] = tot[m];  // the own columns' total, kept in registers
       }
     }
     block_excl_scan(pre, NV, sm);
@@ -335,23 +357,27 @@ __device__ __noinline__ void cta_pair_levels_t(const Geo &G, const double *__res
         R[k] = k < n ? a[k] : 0.0;  // R_1
         lsum[0] += R[k];
       }
-#pragma unroll 1
-      for (int m = 1; m < M; ++m) {
-        double cav[CC];
 #pragma unroll
-        for (int k = 0; k < CC; ++k) cav[k] = k < n ? CA(m - 1, k) : 0.0;
-        double p = pre[m - 1];
+      for (int m = 1; m < MB; ++m) {
+        if (m < M) {
+          double cav[CC];
 #pragma unroll
-        for (int k = 0; k < CC; ++k) {
-          const double Rn = a[k] * p;  // R_{m+1}, S_m = the prefix left of column k
-          lsum[m] += k < n ? Rn : 0.0;
-          p += cav[k];
-          cav[k] += R[k];
-          R[k] = Rn;
+          for (int k = 0; k < CC; ++k) cav[k] = k < n ? CA(m - 1, k) : 0.0;
+          double p = pre[m - 1], rs = 0.0;
+#pragma unroll
+          for (int k = 0; k < CC; ++k) {
+            const double Rn = a[k] * p;  // R_{m+1}, S_m = the prefix left of column k
+            lsum[m] += Rn;               // a[k] = 0 beyond the own cells
+            p += cav[k];
+            cav[k] += R[k];
+            rs += R[k];
+            R[k] = Rn;
+          }
+          tot[m - 1] += rs;
+#pragma unroll
+          for (int k = 0; k < CC; ++k)
+            if (k < n) CA(m - 1, k) = cav[k];
         }
-#pragma unroll
-        for (int k = 0; k < CC; ++k)
-          if (k < n) CA(m - 1, k) = cav[k];
       }
     }
   };
@@ -1165,6 +1191,16 @@ int64_t redo_slot_doubles(int64_t lx, int64_t ly, int64_t d, const sk_kernel_con
   return wide_short(lx, ly, d, c) ? std::max(slot, WB * WSLOT) : slot;
 }
 
+// dynamic shared memory of a row-scan launch: the y staging area, grown to
+// hold the column state of long rows (more than 2 columns per thread) too
+size_t long_row_smem(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
+  const int64_t L = std::max(lx, ly), T = c.difference ? L - 1 : L;
+  const int64_t NV = std::max(c.n_levels - 1, 0), C = (T + RT - 1) / RT;
+  if (d >= 32 || L * d > YSTAGE_BYTES / 8 || C <= 2) return YSTAGE_BYTES;
+  const size_t need = (size_t)((((L * d + 1) & ~1ll) + NV * C * RT) * 8);
+  return need <= (size_t)DYN_SMEM_MAX ? std::max<size_t>(YSTAGE_BYTES, need) : YSTAGE_BYTES;
+}
+
 int64_t grid_for(int64_t work, int64_t slot) {
   // enough CTAs to fill the machine, scratch within 256 MiB
   const int64_t cap = std::max<int64_t>(1, (256ll << 20) / (slot * 8));
@@ -1219,8 +1255,9 @@ int rowscan_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64
   if (!ws || ws_bytes < (size_t)(grid * A.slot * 8))
     return fail(SK_ERR_WORKSPACE, "workspace too small for the float64 row-scan kernel");
   A.scratch = (double *)ws;
-  SK_CHECK_CUDA(cudaFuncSetAttribute(gram_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, YSTAGE_BYTES));
-  gram_kernel<false><<<(unsigned)grid, RT, YSTAGE_BYTES, st>>>(A);
+  const size_t dyn = long_row_smem(lx, mode == 2 ? lx : ly, d, c);
+  SK_CHECK_CUDA(cudaFuncSetAttribute(gram_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  gram_kernel<false><<<(unsigned)grid, RT, dyn, st>>>(A);
   SK_CHECK_LAUNCH();
   return SK_OK;
 }
@@ -1306,8 +1343,8 @@ int cert_fixup(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t
   } else {
     const int64_t grid = std::min<int64_t>(grid_for(1ll << 40, A.slot), (total + RT - 1) / RT);
     SK_CHECK_CUDA(cudaFuncSetAttribute(cert_redo_kernel<false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, YSTAGE_BYTES));
-    cert_redo_kernel<false><<<(unsigned)grid, RT, YSTAGE_BYTES, st>>>(A);
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)long_row_smem(lx, ly, d, c)));
+    cert_redo_kernel<false><<<(unsigned)grid, RT, long_row_smem(lx, ly, d, c), st>>>(A);
   }
   SK_CHECK_LAUNCH();
   return SK_OK;
@@ -1322,8 +1359,9 @@ int cert_self_fixup(const double *X, int64_t n, int64_t l, int64_t d, const sk_k
   const int64_t grid = grid_for(n, slot);
   if (!ws || ws_bytes < (size_t)(grid * slot * 8))
     return fail(SK_ERR_WORKSPACE, "workspace too small for the self-level fix-up");
-  SK_CHECK_CUDA(cudaFuncSetAttribute(self_cert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, YSTAGE_BYTES));
-  self_cert_kernel<<<(unsigned)grid, RT, YSTAGE_BYTES, st>>>(G, out, (double *)ws, slot);
+  const size_t dyn = long_row_smem(l, l, d, c);
+  SK_CHECK_CUDA(cudaFuncSetAttribute(self_cert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  self_cert_kernel<<<(unsigned)grid, RT, dyn, st>>>(G, out, (double *)ws, slot);
   SK_CHECK_LAUNCH();
   return SK_OK;
 }

@@ -1,5 +1,5 @@
-set -x
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
-timeout 300 python tools/devtime.py c4 4096 fp32 2 2>&1 | tail -1
-timeout 900 python tools/bulk_parity.py c4 64 5 2>&1 | tail -1
-timeout 900 python tools/bulk_parity.py c4 64 6 2>&1 | tail -1
+timeout 600 ncu -f --set full --clock-control none --import-source on -k regex:"gram_kernel" -c 1 \
+  -o /tmp/r2_c5_pair python tools/diag_fp64_pair.py c5 > /dev/null 2>&1
+ncu -i /tmp/r2_c5_pair.ncu-rep --page source --csv --print-source sass > /tmp/r2_c5_pair.src.csv 2>/dev/null
+python tools/ncu_summary.py /tmp/r2_c5_pair.ncu-rep > gpurun_out/r2_c5_pair.summary.txt 2>&1
+python tools/ncu_stalls.py /tmp/r2_c5_pair.src.csv 40 >> gpurun_out/r2_c5_pair.summary.txt 2>&1

@@ -1,2 +1,4 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k certification_flags 2>&1 | grep -E "^E|assert|Error" | head -20
-timeout 900 python tools/bulk_parity.py c4 64 6 2>&1 | tail -1
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
+timeout 300 python tools/diag_fp64_pair.py c5 2>&1 | tail -3
+timeout 300 python tools/diag_fp64_pair.py c3 2>&1 | tail -3
+timeout 300 python tools/devtime.py c5 512 fp32 2 | tail -1

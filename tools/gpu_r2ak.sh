@@ -1,6 +1,6 @@
-set -x
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
-timeout 300 python tools/devtime.py c4 4096 fp32 2 2>&1 | tail -1
-for s in 6 7 8 9; do timeout 900 python tools/bulk_parity.py c4 64 $s 2>&1 | tail -1; done
-timeout 300 python tools/diag_fp64_pair.py c4 2>&1 | tail -3
-timeout 300 python tools/devtime.py c4 512 fp64 2 2>&1 | tail -1
+timeout 600 ncu -f --set full --clock-control none --import-source on -k regex:"gram_kernel" -c 1 \
+  -o /tmp/r2_c5_pair python tools/diag_fp64_pair.py c5 > /dev/null 2>&1
+ncu -i /tmp/r2_c5_pair.ncu-rep --page source --csv --print-source cuda,sass > /tmp/r2_c5_pair.cs.csv 2>gpurun_out/cs.err
+ls -la /tmp/r2_c5_pair.cs.csv
+gzip -c /tmp/r2_c5_pair.cs.csv > gpurun_out/r2_c5_pair.cs.csv.gz
+ls -la gpurun_out/
