@@ -438,6 +438,26 @@ def test_pde_golden_gram():
             assert np.array_equal(K, K.T)
 
 
+@pytest.mark.parametrize("lx,ly,d,kind,diff", [
+    (5, 7, 3, "rbf", True), (40, 33, 2, "linear", True), (70, 100, 5, "rbf", True),
+    (150, 200, 3, "matern32", True), (12, 9, 20, "rbf", True), (30, 140, 12, "rbf", False),
+    (300, 280, 2, "rbf", True)])
+def test_pde_shapes_vs_oracle(lx, ly, d, kind, diff):
+    """Warp-per-pair systolic solve (columns per lane 1..8, registers or memory
+    for the points) and the long-sequence thread-per-pair fallback, vs the oracle."""
+    X = gen_brownian(3, lx, d, SeedStream(81)).data
+    Y = gen_brownian(2, ly, d, SeedStream(82)).data
+    kw = {"scale": 0.8} if kind == "linear" else {"bandwidth": 1.1}
+    cfg = KernelConfig(static=StaticKernelSpec(kind=kind, **kw), difference=diff)
+    sp = O.static_params(kind, **kw)
+    K = sig_kernel_gram(X, Y, cfg=cfg, algorithm="pde")
+    rtol = 1e-8 if kind.startswith("matern") else 1e-11
+    assert np.allclose(K, O.pde_gram(X, Y, sp=sp, difference=diff), rtol=rtol, atol=0)
+    Ks = sig_kernel_gram(X, cfg=cfg, algorithm="pde")
+    assert np.array_equal(Ks, Ks.T)
+    assert np.allclose(Ks, O.pde_gram(X, None, sp=sp, difference=diff), rtol=rtol, atol=0)
+
+
 def test_pde_hand_values_and_errors():
     """test_kernels.py:233-262 re-pointed at the device path."""
     from paper_2501_07145_b200 import sig_pde_kernel
