@@ -1006,7 +1006,8 @@ int launch_d16(const Params &, int M, int order, int variant, size_t smem, cudaS
 // Compiled (n_levels, order) combinations: order 1 with n_levels 1..8, and
 // every order 2 <= p <= n_levels for n_levels 2..5 (p = n_levels: geometric).
 __host__ __device__ constexpr bool fast_orders_supported(int M, int order) {
-  return (order == 1 && M >= 1 && M <= 8) || (order >= 2 && order <= M && M <= 5);
+  return (order == 1 && M >= 1 && M <= 8) || (order >= 2 && order <= M && M <= 5) ||
+         (order == 2 && M <= 8) || (order == 3 && M == 6);
 }
 __host__ __device__ constexpr int columns_per_lane(int order) { return order == 1 ? 8 : 4; }
 
@@ -1049,7 +1050,7 @@ int launch_impl_lin(const Params &P, int M, int order, size_t smem, cudaStream_t
 #define SK_G(MM, PP) \
   if (M == MM && order == PP) return launch_kernel<LaneStateG<PointStage<D, 4, LIN>, MM, PP>>(P, smem, st);
     SK_G(2, 2) SK_G(3, 2) SK_G(3, 3) SK_G(4, 2) SK_G(4, 3) SK_G(4, 4)
-    SK_G(5, 2) SK_G(5, 3) SK_G(5, 4) SK_G(5, 5)
+    SK_G(5, 2) SK_G(5, 3) SK_G(5, 4) SK_G(5, 5) SK_G(6, 2) SK_G(6, 3) SK_G(7, 2) SK_G(8, 2)
 #undef SK_G
   }
   return fail(SK_ERR_UNSUPPORTED, "fast path: (n_levels, order) not compiled");

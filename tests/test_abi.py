@@ -51,8 +51,10 @@ def test_fast_path_selection():
     assert lib.sk_fast_path(128, 128, 8, geo) == 1          # geometric p = M (c2)
     mid = _native.config_struct(KernelConfig(n_levels=5, order=3))
     assert lib.sk_fast_path(128, 128, 8, mid) == 1          # 1 < p < M: fused general order
-    big = _native.config_struct(KernelConfig(n_levels=6, order=3))
-    assert lib.sk_fast_path(128, 128, 8, big) == 0          # p > 1 beyond n_levels 5: float64
+    for M, p in ((6, 2), (6, 3), (7, 2), (8, 2)):             # many levels, low order: fused
+        assert lib.sk_fast_path(128, 128, 8, _native.config_struct(KernelConfig(n_levels=M, order=p))) == 1
+    big = _native.config_struct(KernelConfig(n_levels=6, order=4))
+    assert lib.sk_fast_path(128, 128, 8, big) == 0          # register budget exceeded: float64
     lgeo = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="linear"), n_levels=4,
                                               order=4, normalization="levelwise"))
     assert lib.sk_fast_path(64, 64, 4, lgeo) == 0           # normalised linear p > 1: float64

@@ -699,7 +699,8 @@ def test_full_size_baseline_configs(gram_cases, name):
     assert torch.equal(Kb, K[rows])
 
 
-@pytest.mark.parametrize("M,p", [(3, 2), (4, 2), (4, 3), (5, 2), (5, 3), (5, 4)])
+@pytest.mark.parametrize("M,p", [(3, 2), (4, 2), (4, 3), (5, 2), (5, 3), (5, 4),
+                                 (6, 2), (6, 3), (7, 2), (8, 2)])
 def test_intermediate_orders_fused(M, p):
     """1 < p < M (test_kernels.py:143-150 sweeps p = 1..4 at M = 4) on the fused kernel."""
     X = gen_brownian(6, 50, 4, SeedStream(71)).data
@@ -711,6 +712,14 @@ def test_intermediate_orders_fused(M, p):
         assert uses_fast_path(50, 37, 4, cfg)
         R = O.gram(X, Y, sp=O.static_params(kind), M=M, p=p, normalization=norm)
         assert _scaled_err(sig_kernel_gram(X, Y, cfg=cfg), R) <= tol, (kind, norm)
+    if M >= 6:  # multi-panel (L > 128 columns at 4 per lane) and symmetric
+        X = gen_brownian(4, 300, 3, SeedStream(73)).data
+        cfg = KernelConfig(n_levels=M, order=p, normalization="levelwise")
+        assert uses_fast_path(300, 300, 3, cfg)
+        K = sig_kernel_gram(X, cfg=cfg)
+        assert np.array_equal(K, K.T) and np.array_equal(np.diag(K), np.ones(4))
+        R = O.gram(X, None, sp=O.static_params("rbf"), M=M, p=p, normalization="levelwise")
+        assert _scaled_err(K, R) <= TOL_NORM
 
 
 @pytest.mark.parametrize("norm", ["none", "levelwise", "global"])
