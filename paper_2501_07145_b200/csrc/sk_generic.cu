@@ -367,6 +367,129 @@ __global__ void copy_levels_kernel(const double *lv, int64_t count, int M, doubl
   if (t < count * (M + 1)) out[t] = lv[t];
 }
 
+// Lifted DP with precomputed slot Grams, order 1, T' <= 128 (rfsf_exact_gram):
+// one warp per pair, lanes own 4 columns, one warp-level exclusive scan per
+// level and row (the order-1 recursion of pair_levels with a per-level A,
+// features.py:418-424). Every level's slot-Gram row r+1 is read once (the
+// previous row stays in registers) and the next row is requested before the
+// current one is used; the per-pair state lives in registers instead of the
+// pair-fastest workspace of the thread-per-pair kernel.
+constexpr int LW_WARPS = 8;
+
+template <int MB>
+__global__ void __launch_bounds__(32 * LW_WARPS) lifted_warp_kernel(GenParams P) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int M = P.M;
+  const int64_t T1 = P.t1, T2 = P.t2;
+  const bool diff = P.difference;
+  const int c0 = 4 * lane;
+  constexpr int VB = MB - 1;
+  for (int64_t t = (int64_t)blockIdx.x * LW_WARPS + warp; t < P.count;
+       t += (int64_t)gridDim.x * LW_WARPS) {
+    const int64_t g = P.g0 + t;
+    int64_t i, j;
+    pair_of(P, g, i, j);
+    double *out = P.lv + t * (M + 1);
+    if ((P.mode == 1 && j < i) || M == 0 || T1 <= 0 || T2 <= 0) {
+      if (lane == 0) {
+        out[0] = 1.0;
+        for (int m = 1; m <= M; ++m) out[m] = 0.0;
+      }
+      continue;
+    }
+    const double *gx = P.mode == 2 ? P.G + i * P.lx * P.g_ld
+                                   : P.G + ((i - P.g_row0) * P.lx) * P.g_ld + j * P.ly;
+    // G columns c0 .. c0 + 4 of one row of every level (column c0 + 4 for the
+    // double difference of the lane's last cell)
+    const int64_t ncol = diff ? T2 + 1 : T2;
+    double gcur[MB][5], gnx[MB][5];
+    const auto load_row = [&](int64_t r, double (&dst)[MB][5]) {
+#pragma unroll
+      for (int h = 0; h < MB; ++h)
+#pragma unroll
+        for (int k = 0; k < 5; ++k)
+          dst[h][k] = (h < M && r < (diff ? T1 + 1 : T1) && c0 + k < ncol)
+                          ? gx[h * P.g_lvl + r * P.g_ld + c0 + k]
+                          : 0.0;
+    };
+    load_row(0, gcur);
+    if (diff) load_row(1, gnx);
+    double ca[VB > 0 ? VB : 1][4], lsum[MB];
+#pragma unroll
+    for (int m = 0; m < VB; ++m)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ca[m][k] = 0.0;
+#pragma unroll
+    for (int m = 0; m < MB; ++m) lsum[m] = 0.0;
+    for (int64_t r = 0; r < T1; ++r) {
+      double a[MB][4];
+#pragma unroll
+      for (int h = 0; h < MB; ++h)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const bool in = c0 + k < T2;
+          // features.py:418-419: G[1:,1:] - G[:-1,1:] - G[1:,:-1] + G[:-1,:-1]
+          a[h][k] = !in ? 0.0
+                    : diff ? gnx[h][k + 1] - gcur[h][k + 1] - gnx[h][k] + gcur[h][k]
+                           : gcur[h][k];
+        }
+      // advance the row window and request the next row before the recursion
+      if (diff) {
+#pragma unroll
+        for (int h = 0; h < MB; ++h)
+#pragma unroll
+          for (int k = 0; k < 5; ++k) gcur[h][k] = gnx[h][k];
+        load_row(r + 2, gnx);
+      } else {
+        load_row(r + 1, gcur);
+      }
+      double pre[VB > 0 ? VB : 1];
+#pragma unroll
+      for (int m = 0; m < VB; ++m) pre[m] = ca[m][0] + ca[m][1] + ca[m][2] + ca[m][3];
+#pragma unroll
+      for (int m = 0; m < VB; ++m) {
+        if (m + 1 < M) {
+          double inc = pre[m];
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const double u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+          }
+          pre[m] = inc - pre[m];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        double Rprev = a[0][k];
+        lsum[0] += Rprev;
+#pragma unroll
+        for (int m = 1; m < MB; ++m) {
+          if (m < M) {
+            const double Rn = a[m][k] * pre[m - 1];
+            lsum[m] += Rn;
+            pre[m - 1] += ca[m - 1][k];
+            ca[m - 1][k] += Rprev;
+            Rprev = Rn;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MB; ++m) {
+      double v = lsum[m];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      lsum[m] = v;
+    }
+    if (lane == 0) {
+      out[0] = 1.0;
+#pragma unroll
+      for (int m = 0; m < MB; ++m)
+        if (m < M) out[m + 1] = lsum[m];
+    }
+  }
+}
+
 int64_t scratch_slots(int64_t t2, int64_t ly, int M, int p, int lifted = 0) {
   const int64_t mm = std::max(M - 1, 0);
   return mm * t2 * p + (lifted ? std::max(M, 1) : 1) * ly + 1;
@@ -395,7 +518,14 @@ int run_chunks(GenParams P, int64_t npairs, int norm, const double *diag_x,
     P.g0 = g0;
     P.count = std::min(ch, npairs - g0);
     const int blocks = (int)((P.count + GEN_THREADS - 1) / GEN_THREADS);
-    generic_levels_kernel<<<blocks, GEN_THREADS, 0, st>>>(P);
+    if (P.lifted && P.G && P.p == 1 && P.M >= 1 && P.M <= 4 && P.t2 <= 128) {
+      // (n_levels 5-8 would need 8 levels of row windows: 1.6 KB of spills)
+      const unsigned wb = (unsigned)std::min<int64_t>((P.count + LW_WARPS - 1) / LW_WARPS,
+                                                      (int64_t)sm_count() * 16);
+      lifted_warp_kernel<4><<<wb, 32 * LW_WARPS, 0, st>>>(P);
+    } else {
+      generic_levels_kernel<<<blocks, GEN_THREADS, 0, st>>>(P);
+    }
     SK_CHECK_LAUNCH();
     if (self_out) {
       const int64_t n = P.count * (P.M + 1);
