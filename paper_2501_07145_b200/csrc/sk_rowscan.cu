@@ -539,8 +539,16 @@ bool wide_short(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   return p == 1 && d >= 32 && lx <= WP && ly <= WP && c.n_levels <= GEN_MAX_LEVELS;
 }
 
+// linear kind with differences: wide_point_matrix leaves the raw inner
+// products and the double difference applies the scale (the kernel is
+// bilinear, kernels.py:281), saving a pass over the matrix
+__device__ __forceinline__ double wide_dd_scale(const Geo &G) {
+  return G.S.kind == SK_LINEAR && G.difference ? G.S.scale : 1.0;
+}
+
 // The pair's point-kernel matrix Am[r][c] = k(x_r, y_c) (r < lx, c < ly) into
-// shared memory (row stride WPS). All threads call it; Am is complete on return.
+// shared memory (row stride WPS; linear with differences: the raw inner
+// products, see wide_dd_scale). All threads call it; Am is complete on return.
 __device__ __noinline__ void wide_point_matrix(const Geo &G, const double *__restrict__ xs,
                                                int64_t lx, const double *__restrict__ ys,
                                                int64_t ly, double *smem) {
@@ -607,6 +615,7 @@ __device__ __noinline__ void wide_point_matrix(const Geo &G, const double *__res
   // the static kernel in a rolled loop: one copy of its code (inlined into the
   // unrolled tile above it was 64 copies, and the instruction cache missed)
   const StaticF64 S = G.S;
+  if (S.kind == SK_LINEAR && G.difference) return;  // scale applied by the double difference
   for (int r = t / WP; r < R; r += RT / WP) {
     const int c = t % WP;
     if (c < C) {
@@ -713,11 +722,12 @@ __device__ __noinline__ void wide_pair_levels(const Geo &G, const double *__rest
   wide_point_matrix(G, xs, lx, ys, ly, smem);
   const double *Am = smem;
   const bool diff = G.difference;
+  const double sc = wide_dd_scale(G);
   if (warp == 0)
     warp_levels<MB>(
         [&](int i, int c) {
-          return diff ? Am[(i + 1) * WPS + c + 1] - Am[i * WPS + c + 1] - Am[(i + 1) * WPS + c] +
-                            Am[i * WPS + c]
+          return diff ? sc * (Am[(i + 1) * WPS + c + 1] - Am[i * WPS + c + 1] -
+                              Am[(i + 1) * WPS + c] + Am[i * WPS + c])
                       : Am[i * WPS + c];
         },
         T1, T2, M, lane, lv_out);
@@ -1012,12 +1022,13 @@ __device__ __noinline__ void wide_stage_pair(const Geo &G, const double *xs, int
   wide_point_matrix(G, xs, lx, ys, ly, smem);
   const double *Am = smem;
   const bool diff = G.difference;
+  const double sc = wide_dd_scale(G);
   for (int e = threadIdx.x; e < T1 * WP; e += RT) {
     const int i = e / WP, c = e % WP;
     double v = 0.0;
     if (c < T2)
-      v = diff ? Am[(i + 1) * WPS + c + 1] - Am[i * WPS + c + 1] - Am[(i + 1) * WPS + c] +
-                     Am[i * WPS + c]
+      v = diff ? sc * (Am[(i + 1) * WPS + c + 1] - Am[i * WPS + c + 1] - Am[(i + 1) * WPS + c] +
+                       Am[i * WPS + c])
                : Am[i * WPS + c];
     out[e] = v;
   }
@@ -1321,9 +1332,13 @@ int cert_fixup(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t
     corners_kernel<<<(unsigned)std::min<int64_t>((tx + 255) / 256, sm_count() * 8), 256, 0, st>>>(
         X, nx, lx, d, Xc);
     SK_CHECK_LAUNCH();
-    corners_kernel<<<(unsigned)std::min<int64_t>((ty + 255) / 256, sm_count() * 8), 256, 0, st>>>(
-        symmetric ? X : Y, ny, ly, d, Yc);
-    SK_CHECK_LAUNCH();
+    if (symmetric) {
+      Yc = Xc;  // K(X): both roles are X
+    } else {
+      corners_kernel<<<(unsigned)std::min<int64_t>((ty + 255) / 256, sm_count() * 8), 256, 0, st>>>(
+          Y, ny, ly, d, Yc);
+      SK_CHECK_LAUNCH();
+    }
     const int64_t tiles = ((A.rows + SR - 1) / SR) * ((ny + RT - 1) / RT);
     const unsigned g = (unsigned)std::min<int64_t>(tiles, (int64_t)sm_count() * 8);
     const int k = c.static_spec.kind;
