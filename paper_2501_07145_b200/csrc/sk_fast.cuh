@@ -1070,8 +1070,14 @@ int launch_impl_stat(const Params &P, int M, int order, size_t smem, cudaStream_
       case 8: return launch_kernel<LaneState1<StatPointStage<D, 8>, 8>>(P, smem, st);
       default: break;
     }
+  } else {
+#define SK_GS(MM, PP) \
+  if (M == MM && order == PP) return launch_kernel<LaneStateG<StatPointStage<D, 4>, MM, PP>>(P, smem, st);
+    SK_GS(2, 2) SK_GS(3, 2) SK_GS(3, 3) SK_GS(4, 2) SK_GS(4, 3) SK_GS(4, 4)
+    SK_GS(5, 2) SK_GS(5, 3) SK_GS(5, 4) SK_GS(5, 5) SK_GS(6, 2) SK_GS(6, 3) SK_GS(7, 2) SK_GS(8, 2)
+#undef SK_GS
   }
-  return fail(SK_ERR_UNSUPPORTED, "fast path: stationary kinds are compiled for order 1");
+  return fail(SK_ERR_UNSUPPORTED, "fast path: (n_levels, order) not compiled");
 }
 
 // Instantiation helper shared by the per-D translation units.

@@ -64,7 +64,7 @@ def test_fast_path_selection():
     assert lib.sk_fast_path(64, 64, 4, mat) == 1            # stationary kinds, order 1: fused
     matp = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="matern32"), n_levels=3,
                                               order=3))
-    assert lib.sk_fast_path(64, 64, 4, matp) == 0           # stationary kinds, order > 1: float64
+    assert lib.sk_fast_path(64, 64, 4, matp) == 1           # stationary kinds, order > 1: fused
     poly = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="polynomial")))
     assert lib.sk_fast_path(64, 64, 4, poly) == 1           # polynomial, order 1: fused
     poly2 = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="polynomial"),

@@ -590,6 +590,27 @@ def test_stationary_kinds_fused(kind):
     assert _scaled_err(K, O.gram(X, None, sp=sp, M=4, p=1, normalization="levelwise")) <= TOL_NORM
 
 
+@pytest.mark.parametrize("kind,M,p", [("matern12", 3, 2), ("matern32", 4, 4), ("matern52", 5, 3),
+                                      ("rational_quadratic", 5, 5), ("matern32", 8, 2)])
+def test_stationary_kinds_general_order_fused(kind, M, p):
+    """Matern / rational quadratic at 1 < p <= M on the general-order fused kernel."""
+    X = gen_brownian(6, 50, 5, SeedStream(55)).data
+    Y = gen_brownian(5, 41, 5, SeedStream(56)).data
+    extra = dict(alpha=1.3) if kind == "rational_quadratic" else {}
+    spec = StaticKernelSpec(kind=kind, bandwidth=1.1, **extra)
+    sp = O.static_params(kind, bandwidth=1.1, **extra)
+    for norm, tol in (("none", TOL_RAW), ("levelwise", TOL_NORM)):
+        cfg = KernelConfig(static=spec, n_levels=M, order=p, normalization=norm)
+        assert uses_fast_path(50, 41, 5, cfg)
+        R = O.gram(X, Y, sp=sp, M=M, p=p, normalization=norm)
+        assert _scaled_err(sig_kernel_gram(X, Y, cfg=cfg), R) <= tol, (kind, norm)
+    cfg = KernelConfig(static=spec, n_levels=M, order=p, normalization="levelwise")
+    Xl = gen_brownian(3, 300, 3, SeedStream(57)).data  # multi-panel, symmetric
+    K = sig_kernel_gram(Xl, cfg=cfg)
+    assert np.array_equal(K, K.T) and np.array_equal(np.diag(K), np.ones(3))
+    assert _scaled_err(K, O.gram(Xl, None, sp=sp, M=M, p=p, normalization="levelwise")) <= TOL_NORM
+
+
 def test_stationary_kind_multi_panel():
     X = gen_brownian(4, 300, 3, SeedStream(53)).data
     Y = gen_brownian(3, 280, 3, SeedStream(54)).data
