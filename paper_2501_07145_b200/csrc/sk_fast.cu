@@ -196,7 +196,7 @@ Plan plan_for(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   if (c.precision != SK_PREC_FP32) return pl;
   const bool stat = stationary_kind(kind);
   const bool poly = kind == SK_POLYNOMIAL;
-  if (poly && (c.order != 1 || !c.difference)) return pl;  // polynomial: order 1, differenced
+  if (poly && !c.difference) return pl;  // polynomial: differenced only
   pl.nodiff = !c.difference;
   if (pl.nodiff && (stat || (kind == SK_RBF && c.order != 1))) return pl;  // not compiled
   if (!fast_orders_supported(c.n_levels, c.order)) return pl;

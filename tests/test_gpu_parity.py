@@ -641,6 +641,13 @@ def test_polynomial_fused(degree, gamma):
                 continue
             err = _scaled_err(sig_kernel_gram(X, Y, cfg=cfg), R)
             assert err <= tol, (degree, lx, norm, err)
+    for M, p in ((3, 2), (4, 4), (6, 2)):  # general order
+        X = gen_brownian(5, 45, 6, SeedStream(74)).data
+        Y = gen_brownian(4, 38, 6, SeedStream(75)).data
+        cfg = KernelConfig(static=spec, n_levels=M, order=p, normalization="levelwise")
+        assert execution_path(45, 38, 6, cfg) == "fused"
+        R = O.gram(X, Y, sp=sp, M=M, p=p, normalization="levelwise")
+        assert _scaled_err(sig_kernel_gram(X, Y, cfg=cfg), R) <= TOL_NORM, (degree, M, p)
     X = gen_brownian(6, 50, 6, SeedStream(73)).data
     cfg = KernelConfig(static=spec, n_levels=5, normalization="levelwise")
     K = sig_kernel_gram(X, cfg=cfg)
