@@ -1,3 +1,4 @@
+# DRAM bytes (read + write) and duration of the full-size c3 / c5 / c2 Gram launch -> gpurun_out/r2_<cfg>_traffic.csv (profiles/traffic.json)
 set -x
 mkdir -p gpurun_out
 for c in c3 c5 c2; do
