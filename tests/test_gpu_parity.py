@@ -510,7 +510,8 @@ def test_graph_plan_matches_eager_bitwise(norm):
     from paper_2501_07145_b200 import RBFKernel, SignatureKernel
     X = gen_brownian(64, 50, 3, SeedStream(1)).data
     Y = gen_brownian(48, 50, 3, SeedStream(2)).data
-    eager = SignatureKernel(n_levels=5, normalization=norm, static_kernel=RBFKernel())
+    eager = SignatureKernel(n_levels=5, normalization=norm, static_kernel=RBFKernel(),
+                            cuda_graph=False)
     graph = SignatureKernel(n_levels=5, normalization=norm, static_kernel=RBFKernel(),
                             cuda_graph=True)
     for A, B in ((X, None), (X, Y)):
@@ -544,13 +545,36 @@ def test_graph_plan_gemm_path_bitwise(kind):
     Y = gen_brownian(7, 40, 24, SeedStream(6)).data
     static = LinearKernel() if kind == "linear" else RBFKernel()
     norm = "none" if kind == "linear" else "levelwise"
-    eager = SignatureKernel(n_levels=3, normalization=norm, static_kernel=static)
+    eager = SignatureKernel(n_levels=3, normalization=norm, static_kernel=static, cuda_graph=False)
     graph = SignatureKernel(n_levels=3, normalization=norm, static_kernel=static, cuda_graph=True)
     assert execution_path(40, 40, 24, eager.config if hasattr(eager, "config") else
                           KernelConfig(static=StaticKernelSpec(kind=kind), n_levels=3,
                                        normalization=norm)) == "gemm"
     for A, B in ((X, Y), (X, None), (X + 0.02, Y)):
         assert np.array_equal(graph(A, B), eager(A, B))
+
+
+def test_facade_auto_graph_for_launch_bound_calls():
+    """cuda_graph='auto' (the default): small Grams replay a captured plan, bitwise
+    equal to the eager call; large ones, other devices' tensors and SequenceBatch
+    inputs stay eager; errors keep the eager messages."""
+    from paper_2501_07145_b200 import RBFKernel, SignatureKernel
+    auto = SignatureKernel(n_levels=5, static_kernel=RBFKernel())
+    eager = SignatureKernel(n_levels=5, static_kernel=RBFKernel(), cuda_graph=False)
+    X = gen_brownian(64, 50, 3, SeedStream(21)).data
+    Xt = torch.from_numpy(X).cuda()
+    assert np.array_equal(auto(X), eager(X))
+    assert torch.equal(auto(Xt), eager(Xt))
+    assert len(auto._plans) == 1  # one plan per shape, numpy or tensor inputs
+    big = torch.zeros((1024, 256, 3), dtype=torch.float64, device="cuda")
+    assert not auto._use_graph(big, None)
+    assert not auto._use_graph(np.zeros((4, 1, 3)), None)  # no increments
+    bad = X.copy()
+    bad[1, 3, 0] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        auto(bad)
+    with pytest.raises(ValueError):
+        SignatureKernel(cuda_graph="sometimes")
 
 
 def test_graph_plan_errors():
