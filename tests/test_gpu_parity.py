@@ -856,6 +856,31 @@ def test_certification_fixup_recomputes_in_float64():
     assert _rel(K, R) <= TOL_NORM
 
 
+@pytest.mark.parametrize("norm", ["none", "levelwise"])
+def test_certification_wide_batched_redo(norm):
+    """GEMM-fed path (d = 40): flagged entries are recomputed by the batched
+    wide-pair float64 redo (both self pairs too when normalised) and equal the
+    float64 kernel's values."""
+    from paper_2501_07145_b200 import _native
+    from paper_2501_07145_b200.kernels import execution_path, gram_block
+    X = gen_brownian(12, 48, 40, SeedStream(91)).data
+    # y ~ -x: the linear kernel's normalised levels alternate in sign and the
+    # levelwise mean cancels to ~0 (flagged); plus unrelated sequences
+    noise = 0.01 * gen_brownian(6, 48, 40, SeedStream(93)).data
+    Y = np.concatenate([-X[:6] + noise, gen_brownian(5, 48, 40, SeedStream(92)).data])
+    cfg = KernelConfig(static=StaticKernelSpec(kind="linear"), n_levels=3, normalization=norm)
+    assert execution_path(48, 48, 40, cfg) == "gemm"
+    Xt, Yt = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
+    K0, lv = gram_block(Xt, Yt, cfg, flags=_native.SK_FLAG_NO_FIXUP, want_levels=True)
+    flagged = _cancellation_flags(K0, lv, "linear", norm).cpu().numpy()
+    assert flagged.any()
+    K = sig_kernel_gram(X, Y, cfg=cfg)
+    K64 = sig_kernel_gram(X, Y, cfg=cfg, precision="fp64")
+    assert np.allclose(K[flagged], K64[flagged], rtol=1e-12, atol=0)
+    R = O.gram(X, Y, sp=O.static_params("linear"), M=3, p=1, normalization=norm)
+    assert _scaled_err(K, R) <= (TOL_RAW if norm == "none" else TOL_NORM)
+
+
 @pytest.mark.parametrize("offset", [50.0, -1e3])
 @pytest.mark.parametrize("kind,d", [("rbf", 8), ("rbf", 16), ("matern32", 4), ("rbf", 40)])
 def test_offset_inputs(offset, kind, d):
