@@ -46,6 +46,8 @@ def test_fast_path_selection():
     lin = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="linear"), n_levels=3))
     assert lib.sk_fast_path(128, 128, 16, lin) == 1
     assert lib.sk_fast_path(128, 128, 128, lin) == 2        # d > 16: GEMM-fed path (c4)
+    geo24 = _native.config_struct(KernelConfig(n_levels=5, order=3))
+    assert lib.sk_fast_path(64, 64, 24, geo24) == 2         # GEMM-fed, 1 < p < M
     assert lib.sk_fast_path(1000, 1000, 16, lin) == 2       # x ring too large for shared memory
     geo = _native.config_struct(KernelConfig(n_levels=5, order=5))
     assert lib.sk_fast_path(128, 128, 8, geo) == 1          # geometric p = M (c2)

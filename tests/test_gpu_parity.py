@@ -272,7 +272,7 @@ def test_gemm_path_linear_c4_shapes():
 
 
 @pytest.mark.parametrize("kind", ["rbf", "linear"])
-@pytest.mark.parametrize("M,p", [(4, 1), (3, 3)])
+@pytest.mark.parametrize("M,p", [(4, 1), (3, 3), (4, 2), (5, 3), (8, 2)])
 def test_gemm_path_kinds_orders(kind, M, p):
     from paper_2501_07145_b200.kernels import execution_path
     X = gen_brownian(7, 70, 24, SeedStream(31)).data
