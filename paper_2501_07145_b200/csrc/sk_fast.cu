@@ -198,7 +198,7 @@ Plan plan_for(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   const bool poly = kind == SK_POLYNOMIAL;
   if (poly && !c.difference) return pl;  // polynomial: differenced only
   pl.nodiff = !c.difference;
-  if (pl.nodiff && (stat || (kind == SK_RBF && c.order != 1))) return pl;  // not compiled
+  if (pl.nodiff && stat) return pl;  // not compiled
   if (!fast_orders_supported(c.n_levels, c.order)) return pl;
   // Normalised linear kernels of order > 1 are sensitive to the FP32
   // accumulation of the increment inner products (measured 1.6-2.1e-5 vs the

@@ -1029,10 +1029,9 @@ int launch_kernel(const Params &P, size_t smem, cudaStream_t st) {
 }
 
 // variant: 0 rbf, 1 linear, 2 stationary kinds (StatPointStage, order 1 only),
-// 3 rbf with difference=False (order 1 only), 4 polynomial
+// 3 rbf with difference=False, 4 polynomial
 template <int D, int LIN>
 int launch_impl_lin(const Params &P, int M, int order, size_t smem, cudaStream_t st) {
-  if (LIN == 2 && order != 1) return fail(SK_ERR_UNSUPPORTED, "fast path: order not compiled");
   if (order == 1) {
     switch (M) {
       case 1: return launch_kernel<LaneState1<PointStage<D, 8, LIN>, 1>>(P, smem, st);
@@ -1045,7 +1044,7 @@ int launch_impl_lin(const Params &P, int M, int order, size_t smem, cudaStream_t
       case 8: return launch_kernel<LaneState1<PointStage<D, 8, LIN>, 8>>(P, smem, st);
       default: break;
     }
-  } else if (LIN != 2) {
+  } else {
 #define SK_G(MM, PP) \
   if (M == MM && order == PP) return launch_kernel<LaneStateG<PointStage<D, 4, LIN>, MM, PP>>(P, smem, st);
     SK_G(2, 2) SK_G(3, 2) SK_G(3, 3) SK_G(4, 2) SK_G(4, 3) SK_G(4, 4)

@@ -685,7 +685,7 @@ def test_difference_false_fused(kind):
     X = gen_brownian(6, 40, 3, SeedStream(61)).data
     Y = gen_brownian(5, 33, 3, SeedStream(62)).data
     sp = O.static_params(kind)
-    orders = (1, 3) if kind == "linear" else (1,)
+    orders = (1, 3) if kind == "linear" else (1, 2, 3)
     for p in orders:
         for norm, tol in (("none", TOL_RAW), ("levelwise", TOL_NORM)):
             if kind == "linear" and p > 1 and norm != "none":
