@@ -100,8 +100,6 @@ struct Params {
   // stationary static kinds (StatPointStage): kind and rational-quadratic alpha
   int static_kind;
   float rq_alpha;
-  float poly_gamma;  // polynomial kind (PointStage KIND 3)
-  int poly_degree;
   // GEMM-fed path (sk_gemm.cu): pair (x, y) row r of the cell matrix is at
   // S + (x - x_blk0) * s_xstride + y * s_ystride + r * s_ld
   const float *S;
@@ -285,13 +283,10 @@ __device__ __forceinline__ void double_difference(const float (&ga)[C], const fl
 // ---------------------------------------------------------------------------
 // KIND 0: rbf, double-differenced (kernels.py:281); 1: linear (the packed values
 // are increments, or points when difference=False: A is the point kernel
-// itself); 2: rbf with difference=False (A = G); 3: polynomial
-// (scale <x, y> + gamma)^degree (static/kernels.py:68-71) on points pre-scaled
-// by sqrt(scale), double-differenced.
+// itself); 2: rbf with difference=False (A = G).
 template <int D, int C_, int KIND>
 struct PointStage {
   static constexpr bool LINEAR = KIND == 1;
-  static constexpr bool POLY = KIND == 3;
   static constexpr int C = C_;
   static constexpr int XP = x_stride(D);
   static constexpr int YP = y_stride(D);
@@ -301,13 +296,7 @@ struct PointStage {
   float prevG[C];
   float lastDa, lastDb;
   float ga[C], gb[C];  // point-kernel rows a, b of the current row pair
-  float gam;           // polynomial offset
-  int deg;             // polynomial degree
-
-  __device__ __forceinline__ void configure(const Params &P) {
-    gam = P.poly_gamma;
-    deg = P.poly_degree;
-  }
+  __device__ __forceinline__ void configure(const Params &) {}
 
   // this lane's columns of the packed y sequence (pre-scaled points, n-terms)
   __device__ __forceinline__ void load_y(const float *__restrict__ yp) {
@@ -321,7 +310,7 @@ struct PointStage {
         yv[c][4 * k4 + 2] = v.z;
         yv[c][4 * k4 + 3] = v.w;
       }
-      yn[c] = (LINEAR || POLY) ? 0.f : __ldg(yp + c * YP + D);
+      yn[c] = LINEAR ? 0.f : __ldg(yp + c * YP + D);
       prevG[c] = 0.f;
     }
     lastDa = lastDb = 0.f;
@@ -330,7 +319,7 @@ struct PointStage {
   // Point kernel of rows a, b of the row pair at `xptr` (packed FFMA2) -> ga, gb.
   __device__ __forceinline__ void point(const float *__restrict__ xptr) {
     u64 acc[C];
-    if (LINEAR || POLY) {
+    if (LINEAR) {
 #pragma unroll
       for (int c = 0; c < C; ++c) acc[c] = 0ull;
     } else {
@@ -356,15 +345,6 @@ struct PointStage {
       if (LINEAR) {
         ga[c] = lo;
         gb[c] = hi;
-      } else if (POLY) {
-        const float ta = lo + gam, tb = hi + gam;
-        float pa = ta, pb = tb;
-        for (int k = 1; k < deg; ++k) {
-          pa *= ta;
-          pb *= tb;
-        }
-        ga[c] = pa;
-        gb[c] = pb;
       } else if constexpr (D >= 8) {
         // No clamp of the exponent at 0 (the reference clamps the float64
         // squared distance, static/kernels.py:108-114): in FP32 the norm-
@@ -384,8 +364,7 @@ struct PointStage {
 
   __device__ __forceinline__ void increments(float dla, float dlb, bool zero_left, float (&aa)[C],
                                              float (&ab)[C]) {
-    double_difference<C, KIND == 1 || KIND == 2>(ga, gb, prevG, lastDa, lastDb, dla, dlb,
-                                                  zero_left, aa, ab);
+    double_difference<C, KIND != 0>(ga, gb, prevG, lastDa, lastDb, dla, dlb, zero_left, aa, ab);
   }
 };
 
@@ -1029,7 +1008,7 @@ int launch_kernel(const Params &P, size_t smem, cudaStream_t st) {
 }
 
 // variant: 0 rbf, 1 linear, 2 stationary kinds (StatPointStage, order 1 only),
-// 3 rbf with difference=False, 4 polynomial
+// 3 rbf with difference=False
 template <int D, int LIN>
 int launch_impl_lin(const Params &P, int M, int order, size_t smem, cudaStream_t st) {
   if (order == 1) {
@@ -1082,7 +1061,6 @@ int launch_impl_stat(const Params &P, int M, int order, size_t smem, cudaStream_
 template <int D>
 int launch_impl(const Params &P, int M, int order, int variant, size_t smem, cudaStream_t st) {
   if (variant == 2) return launch_impl_stat<D>(P, M, order, smem, st);
-  if (variant == 4) return launch_impl_lin<D, 3>(P, M, order, smem, st);
   if (variant == 3) return launch_impl_lin<D, 2>(P, M, order, smem, st);
   return variant == 1 ? launch_impl_lin<D, 1>(P, M, order, smem, st)
                       : launch_impl_lin<D, 0>(P, M, order, smem, st);

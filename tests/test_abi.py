@@ -68,10 +68,10 @@ def test_fast_path_selection():
                                               order=3))
     assert lib.sk_fast_path(64, 64, 4, matp) == 1           # stationary kinds, order > 1: fused
     poly = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="polynomial")))
-    assert lib.sk_fast_path(64, 64, 4, poly) == 1           # polynomial, order 1: fused
+    assert lib.sk_fast_path(64, 64, 4, poly) == 0           # polynomial: float64
     poly2 = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="polynomial"),
                                                n_levels=3, order=2))
-    assert lib.sk_fast_path(64, 64, 4, poly2) == 1          # polynomial, order > 1: fused
+    assert lib.sk_fast_path(64, 64, 4, poly2) == 0          # polynomial, order > 1: float64
     assert lib.sk_fast_path(300, 300, 4, c3) == 1           # two 256-column panels
     assert lib.sk_fast_path(2048, 2048, 4, _native.config_struct(KernelConfig(n_levels=8))) == 1  # c5
     assert lib.sk_fast_path(1000, 1000, 16, c3) == 2        # x ring would exceed shared memory
