@@ -76,6 +76,10 @@ bool use_rowscan(int64_t lx, int64_t ly, const sk_kernel_config &c) {
   return rowscan_supported(lx, ly, c) && T2 >= 32;
 }
 
+int effective_order(const sk_kernel_config &c) {
+  return std::max(1, std::min(c.order, std::max(c.n_levels, 1)));
+}
+
 int self_fixup(const double *X, int64_t n, int64_t l, int64_t d, const sk_kernel_config &c,
                double *out, void *ws, size_t ws_bytes, cudaStream_t st) {
   if (rowscan_supported(l, l, c)) return cert_self_fixup(X, n, l, d, c, out, ws, ws_bytes, st);
@@ -116,6 +120,8 @@ size_t sk_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int64_
     // (Gram: after the FP32 level-1 buffer of the certification)
     const int64_t l2e = n2 > 0 ? l2 : l1;
     const int64_t n2e = n2 > 0 ? n2 : n1;
+    if (n2 == 0 && effective_order(*cfg) > 1 && (path == 1 || path == 2))  // float64 self levels
+      return generic_workspace_bytes(n1, l1, l1, *cfg);
     const size_t fix = rowscan_supported(l1, l2e, *cfg)
                            ? cert_workspace_bytes(n1, l1, n2e, l2e, d, *cfg)
                            : fixup_workspace_bytes(l1, l2e, *cfg);
@@ -142,6 +148,15 @@ int sk_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
   if (n > 0 && !out) return fail(SK_ERR_INVALID, "out is NULL");
   cudaStream_t st = (cudaStream_t)stream;
   const bool fix = !(cfg->flags & SK_FLAG_NO_FIXUP);
+  // General order (p > 1): the FP32 self levels' high levels carry up to ~2e-5
+  // relative error on short sequences (tools/path_sweep.py), which the
+  // normalisation passes on to every entry of the row; they are N sequences,
+  // not N^2 pairs, so they are computed in float64 outright.
+  if (fix && effective_order(*cfg) > 1 && cfg->precision == SK_PREC_FP32 &&
+      (fast_supported(l, l, d, *cfg) || gemm_supported(l, l, d, *cfg))) {
+    if ((rc = check_generic_limits(*cfg))) return rc;
+    return generic_self_levels(X, n, l, d, *cfg, out, workspace, workspace_bytes, st);
+  }
   if (fast_supported(l, l, d, *cfg)) {
     rc = fast_self_levels(X, n, l, d, *cfg, out, workspace, workspace_bytes, st);
     if (!rc && fix) rc = self_fixup(X, n, l, d, *cfg, out, workspace, workspace_bytes, st);
