@@ -120,14 +120,18 @@ size_t sk_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int64_
     // (Gram: after the FP32 level-1 buffer of the certification)
     const int64_t l2e = n2 > 0 ? l2 : l1;
     const int64_t n2e = n2 > 0 ? n2 : n1;
-    if (n2 == 0 && effective_order(*cfg) > 1 && (path == 1 || path == 2))  // float64 self levels
-      return generic_workspace_bytes(n1, l1, l1, *cfg);
+    // float64 self levels at general order (sk_self_levels), unless SK_FLAG_NO_FIXUP
+    const size_t self64 = (n2 == 0 && effective_order(*cfg) > 1 && (path == 1 || path == 2))
+                              ? generic_workspace_bytes(n1, l1, l1, *cfg)
+                              : 0;
     const size_t fix = rowscan_supported(l1, l2e, *cfg)
                            ? cert_workspace_bytes(n1, l1, n2e, l2e, d, *cfg)
                            : fixup_workspace_bytes(l1, l2e, *cfg);
     const size_t k1 = n2 > 0 ? k1buf_bytes(n1, n2, cfg->normalization) : 0;
-    if (path == 1) return k1 + std::max(fix, fast_workspace_bytes(n1, l1, n2, l2, d, *cfg));
-    if (path == 2) return k1 + std::max(fix, gemm_workspace_bytes(n1, l1, n2, l2, d, *cfg));
+    if (path == 1)
+      return std::max(self64, k1 + std::max(fix, fast_workspace_bytes(n1, l1, n2, l2, d, *cfg)));
+    if (path == 2)
+      return std::max(self64, k1 + std::max(fix, gemm_workspace_bytes(n1, l1, n2, l2, d, *cfg)));
     return n2 > 0 ? std::max(generic_workspace_bytes(n1 * n2, l1, l2, *cfg),
                              rowscan_workspace_bytes(n1 * n2, l1, l2, *cfg))
                   : std::max(generic_workspace_bytes(n1, l1, l1, *cfg),

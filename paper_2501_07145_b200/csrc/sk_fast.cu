@@ -211,6 +211,11 @@ Plan plan_for(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   // (x_T - x_0)^m/m! from terms of size (sum |dx|)^m/m!); the FP32 sweep
   // measured 1.7e-5 normalised: float64 kernel
   if (d < 2 || d > 16 || lx < lmin || ly < lmin) return pl;
+  // d = 2 at general order (non-linear kinds, differenced): the high levels of
+  // nearly planar increments cancel internally, which the certification does
+  // not see; tools/path_sweep.py measured up to 4.8x the levelwise bar there
+  // and <= 0.64x at d >= 3: float64 kernel
+  if (d == 2 && c.order > 1 && c.n_levels > 1 && kind != SK_LINEAR && c.difference) return pl;
   pl.D = d <= 4 ? 4 : (d <= 8 ? 8 : 16);
   const int C = pl.C = columns_per_lane(c.order);
   if (ly <= 32 * C) {

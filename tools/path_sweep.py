@@ -48,7 +48,7 @@ for seed in range(first, first + (int(sys.argv[1]) if len(sys.argv) > 1 else 200
     err = float((np.abs(K - K6) / np.maximum(np.abs(K6), 1e-12 * np.abs(K6).max())).max())
     tol = 1e-4 if norm == "none" else 1e-5
     key = (kind if not kind.startswith("matern") else "matern", path, "p1" if p == 1 else "p>1",
-           "diff" if diff else "nodiff")
+           "diff" if diff else "nodiff", "d2" if d == 2 else "d>2")
     if err / tol > worst.get(key, (0, None))[0]:
         worst[key] = (err / tol, (seed, M, p, norm, d, lx, ly, err))
 print("cases on FP32 paths:", n)
