@@ -96,6 +96,8 @@ Plan plan_for(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   if (!fast::fast_orders_supported(c.n_levels, c.order)) return pl;
   if (kind == SK_LINEAR && c.order > 1 && c.normalization != SK_NORM_NONE) return pl;
   if (d < 2 || lx < 2 || ly < 2) return pl;  // d = 1: float64 (see sk_fast.cu plan_for)
+  // d = 2 at general order, rbf: float64 (see sk_fast.cu plan_for)
+  if (d == 2 && c.order > 1 && c.n_levels > 1 && kind != SK_LINEAR) return pl;
   pl.linear = kind == SK_LINEAR;
   pl.K = (int)((pl.linear ? d : d + 2) + 3) / 4 * 4;
   const int C = pl.C = fast::columns_per_lane(c.order);

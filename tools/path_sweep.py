@@ -1,5 +1,5 @@
 """FP32 paths vs float64 over random configurations: worst error / tolerance per
-(kind, path, order class) (development; python tools/path_sweep.py [cases] [first seed])."""
+(kind, path, order class) (development; python tools/path_sweep.py [cases] [first seed] [long])."""
 import os
 import sys
 
@@ -14,6 +14,7 @@ from paper_2501_07145_b200.kernels import execution_path, gram_block  # noqa: E4
 KINDS = ("rbf", "linear", "matern12", "matern32", "matern52", "rational_quadratic")
 worst, n = {}, 0
 first = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+LONG = len(sys.argv) > 3 and sys.argv[3] == "long"
 for seed in range(first, first + (int(sys.argv[1]) if len(sys.argv) > 1 else 2000)):
     r = np.random.default_rng(9000 + seed)
     kind = KINDS[int(r.integers(0, len(KINDS)))]
@@ -25,6 +26,8 @@ for seed in range(first, first + (int(sys.argv[1]) if len(sys.argv) > 1 else 200
     lx, ly = int(r.integers(2, 120)), int(r.integers(2, 120))
     if r.random() < 0.3:
         lx, ly = int(r.integers(6, 30)), int(r.integers(6, 30))
+    if LONG:  # multi-panel rows and long x rings
+        lx, ly = int(r.integers(120, 700)), int(r.integers(120, 700))
     kw = {}
     if kind != "linear":
         kw["bandwidth"] = float(r.uniform(0.4, 2.0))
