@@ -34,6 +34,11 @@ cases = [
      KernelConfig(static=StaticKernelSpec(kind="linear"), n_levels=3)),
     ("fused rbf M=8 short", gen_brownian(6, 12, 2, SeedStream(10)).data,
      gen_brownian(5, 12, 2, SeedStream(11)).data, KernelConfig(n_levels=8, normalization="levelwise")),
+    ("fused matern32 (4,2)", X, Y, KernelConfig(static=StaticKernelSpec(kind="matern32"),
+                                                n_levels=4, order=2, normalization="levelwise")),
+    ("fused rbf nodiff (3,2)", X, Y, KernelConfig(n_levels=3, order=2, difference=False)),
+    ("gemm rbf d=20 (5,3)", gen_brownian(5, 40, 20, SeedStream(5)).data,
+     gen_brownian(4, 40, 20, SeedStream(6)).data, KernelConfig(n_levels=5, order=3)),
 ]
 fp64_cases = [
     ("fp64 row-scan long rows", gen_brownian(2, 600, 2, SeedStream(12)).data,
