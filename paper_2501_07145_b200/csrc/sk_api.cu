@@ -76,6 +76,8 @@ bool use_rowscan(int64_t lx, int64_t ly, const sk_kernel_config &c) {
   return rowscan_supported(lx, ly, c) && T2 >= 32;
 }
 
+constexpr int64_t SELF64_MAX_L = 32;  // float64 general-order self levels up to this length
+
 int effective_order(const sk_kernel_config &c) {
   return std::max(1, std::min(c.order, std::max(c.n_levels, 1)));
 }
@@ -121,7 +123,8 @@ size_t sk_workspace_bytes(int64_t nx, int64_t lx, int64_t ny, int64_t ly, int64_
     const int64_t l2e = n2 > 0 ? l2 : l1;
     const int64_t n2e = n2 > 0 ? n2 : n1;
     // float64 self levels at general order (sk_self_levels), unless SK_FLAG_NO_FIXUP
-    const size_t self64 = (n2 == 0 && effective_order(*cfg) > 1 && (path == 1 || path == 2))
+    const size_t self64 = (n2 == 0 && effective_order(*cfg) > 1 && l1 <= SELF64_MAX_L &&
+                           (path == 1 || path == 2))
                               ? generic_workspace_bytes(n1, l1, l1, *cfg)
                               : 0;
     const size_t fix = rowscan_supported(l1, l2e, *cfg)
@@ -152,12 +155,13 @@ int sk_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
   if (n > 0 && !out) return fail(SK_ERR_INVALID, "out is NULL");
   cudaStream_t st = (cudaStream_t)stream;
   const bool fix = !(cfg->flags & SK_FLAG_NO_FIXUP);
-  // General order (p > 1): the FP32 self levels' high levels carry up to ~2e-5
-  // relative error on short sequences (tools/path_sweep.py), which the
-  // normalisation passes on to every entry of the row; they are N sequences,
-  // not N^2 pairs, so they are computed in float64 outright.
+  // General order (p > 1), short sequences: the FP32 self levels' high levels
+  // carried up to ~2e-5 relative error at L = 13 (tools/path_sweep.py), which
+  // the normalisation passes on to every entry of the row; up to SELF64_MAX_L
+  // points the float64 kernel costs little (the thread-per-pair kernel at
+  // L = 128 would be 8x the Gram's time), so they are computed in float64.
   if (fix && effective_order(*cfg) > 1 && cfg->precision == SK_PREC_FP32 &&
-      (fast_supported(l, l, d, *cfg) || gemm_supported(l, l, d, *cfg))) {
+      l <= SELF64_MAX_L && (fast_supported(l, l, d, *cfg) || gemm_supported(l, l, d, *cfg))) {
     if ((rc = check_generic_limits(*cfg))) return rc;
     return generic_self_levels(X, n, l, d, *cfg, out, workspace, workspace_bytes, st);
   }

@@ -640,8 +640,9 @@ struct LaneState1 : Stage {
 
 // ---------------------------------------------------------------------------
 // Order p = 1 with float64 column accumulators, row prefixes and level sums
-// (single panel only). The GEMM-fed linear path (large d, e.g. BASELINE c4):
-// its levels are long sums of increment products that cancel, and the FP32
+// (single panel only). The GEMM-fed path (large d, e.g. BASELINE c4; rbf too
+// since a fuzz seed at n_levels 8 sat at 1.06x the bar): its levels are long
+// sums of increment products that cancel, and the FP32
 // accumulation measured up to 5e-5 of sum_m |k_m| there (2e-3 relative on
 // 0.4% of c4's entries); float64 accumulation brings it to ~1e-6 (the FP32
 // cell values remain). The DP of this path streams its cells from HBM

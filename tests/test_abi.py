@@ -46,8 +46,10 @@ def test_fast_path_selection():
     lin = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="linear"), n_levels=3))
     assert lib.sk_fast_path(128, 128, 16, lin) == 1
     assert lib.sk_fast_path(128, 128, 128, lin) == 2        # d > 16: GEMM-fed path (c4)
-    geo24 = _native.config_struct(KernelConfig(n_levels=5, order=3))
+    geo24 = _native.config_struct(KernelConfig(static=StaticKernelSpec(kind="linear"), n_levels=5,
+                                               order=3))
     assert lib.sk_fast_path(64, 64, 24, geo24) == 2         # GEMM-fed, 1 < p < M
+    assert lib.sk_fast_path(64, 64, 24, _native.config_struct(KernelConfig())) == 0  # rbf d > 16
     assert lib.sk_fast_path(1000, 1000, 16, lin) == 2       # x ring too large for shared memory
     geo = _native.config_struct(KernelConfig(n_levels=5, order=5))
     assert lib.sk_fast_path(128, 128, 8, geo) == 1          # geometric p = M (c2)
@@ -74,7 +76,7 @@ def test_fast_path_selection():
     assert lib.sk_fast_path(64, 64, 4, poly2) == 0          # polynomial, order > 1: float64
     assert lib.sk_fast_path(300, 300, 4, c3) == 1           # two 256-column panels
     assert lib.sk_fast_path(2048, 2048, 4, _native.config_struct(KernelConfig(n_levels=8))) == 1  # c5
-    assert lib.sk_fast_path(1000, 1000, 16, c3) == 2        # x ring would exceed shared memory
+    assert lib.sk_fast_path(1000, 1000, 16, c3) == 0        # rbf, x ring beyond shared memory: float64
     assert lib.sk_fast_path(2, 256, 4, c3) == 0             # x shorter than the wavefront
 
 
