@@ -2,7 +2,7 @@
 (kind, path, order class, difference, d class) (development; also the case
 generator of tests/test_gpu_path_sweep.py).
 
-    python tools/path_sweep.py [cases] [first seed] [long]
+    python tools/path_sweep.py [cases] [first seed] [long | smallbw]
 """
 import os
 import sys
@@ -18,7 +18,7 @@ from paper_2501_07145_b200.kernels import execution_path, gram_block  # noqa: E4
 KINDS = ("rbf", "linear", "matern12", "matern32", "matern52", "rational_quadratic")
 
 
-def make_case(seed, long=False):
+def make_case(seed, long=False, small_bw=False):
     """(cfg, d, lx, ly, description) of sweep case `seed`."""
     r = np.random.default_rng(9000 + seed)
     kind = KINDS[int(r.integers(0, len(KINDS)))]
@@ -35,6 +35,8 @@ def make_case(seed, long=False):
     kw = {}
     if kind != "linear":
         kw["bandwidth"] = float(r.uniform(0.4, 2.0))
+        if small_bw:  # points far apart on the kernel's scale
+            kw["bandwidth"] = float(r.uniform(0.05, 0.4))
     else:
         kw["scale"] = float(r.uniform(0.3, 1.5))
     if kind == "rational_quadratic":
@@ -44,10 +46,10 @@ def make_case(seed, long=False):
     return cfg, d, lx, ly, (kind, M, p, norm, diff, d, lx, ly)
 
 
-def run_case(seed, long=False):
+def run_case(seed, long=False, small_bw=False):
     """(path, error / tolerance, description); path None when the case is not
     on an FP32 path or its global normalisation is undefined."""
-    cfg, d, lx, ly, desc = make_case(seed, long)
+    cfg, d, lx, ly, desc = make_case(seed, long, small_bw)
     path = execution_path(lx, ly, d, cfg)
     if path == "fp64":
         return None, 0.0, desc
@@ -67,9 +69,10 @@ def main():
     count = int(sys.argv[1]) if len(sys.argv) > 1 else 2000
     first = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     long = len(sys.argv) > 3 and sys.argv[3] == "long"
+    small_bw = len(sys.argv) > 3 and sys.argv[3] == "smallbw"
     worst, n = {}, 0
     for seed in range(first, first + count):
-        path, ratio, desc = run_case(seed, long)
+        path, ratio, desc = run_case(seed, long, small_bw)
         if path is None:
             continue
         n += 1
