@@ -26,6 +26,10 @@ constexpr int RT = 256;            // threads per CTA
 constexpr int NW = RT / 32;
 constexpr int CMAX = 16;           // columns per thread: T2 <= 4096 (cta_pair_levels_t)
 constexpr int VMAX = GEN_MAX_LEVELS - 1;  // scanned levels (1..M-1)
+// channel count above which the point kernel is a block DGEMM (the cells of
+// 16-row blocks, or of a whole short pair) instead of per-cell dot products:
+// rbf at d = 24 ran 3x slower per cell than at d = 40 on the per-cell form
+constexpr int WIDE_D = 16;
 constexpr int YSTAGE_BYTES = 96 * 1024;   // dynamic shared memory: y staging / wide blocks
 constexpr int WR = 16, KW = 16;           // wide path: point-kernel rows per block, channels per stage
 constexpr int WIDE_COLS = (YSTAGE_BYTES / 8 - WR * KW - RT * (KW + 1)) / WR;  // max columns of a block
@@ -247,10 +251,10 @@ __device__ __noinline__ void cta_pair_levels_t(const Geo &G, const double *__res
 #pragma unroll
   for (int m = 0; m < VB; ++m) tot[m] = 0.0;
   double *smb = sm + NW * VMAX;  // warp-boundary point-kernel values
-  // d >= 32: a row's point-kernel values are formed warp-cooperatively (lanes
+  // d > WIDE_D: a row's point-kernel values are formed warp-cooperatively (lanes
   // over channels: coalesced reads of every y point) into a row buffer in the
   // scratch slice; otherwise every thread evaluates its own columns
-  const bool wide = d >= 32;
+  const bool wide = d > WIDE_D;
   double *grow = colacc;
   const bool inner = G.S.kind == SK_LINEAR || G.S.kind == SK_POLYNOMIAL;
   const int64_t ncol = G.difference ? T2 + 1 : T2;
@@ -508,7 +512,7 @@ __device__ __noinline__ void cta_pair_levels(const Geo &G, const double *__restr
 #undef SK_RS
 }
 
-// --- wide short pairs (d >= 32, L <= 128): block DGEMM + one-warp DP --------
+// --- wide short pairs (d > WIDE_D, L <= 128): block DGEMM + one-warp DP ------
 // The redo of the GEMM-fed path's flagged entries (c4: ~6% of a 4096^2 Gram)
 // is float64 GEMM work: 2.1 M FMAs per pair at d = 128. One CTA forms the
 // pair's whole point-kernel matrix in shared memory with a register-blocked
@@ -536,7 +540,7 @@ __device__ __forceinline__ void cp_async_wait8() {
 
 bool wide_short(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   const int p = std::max(1, std::min(c.order, std::max(c.n_levels, 1)));
-  return p == 1 && d >= 32 && lx <= WP && ly <= WP && c.n_levels <= GEN_MAX_LEVELS;
+  return p == 1 && d > WIDE_D && lx <= WP && ly <= WP && c.n_levels <= GEN_MAX_LEVELS;
 }
 
 // linear kind with differences: wide_point_matrix leaves the raw inner
@@ -1191,7 +1195,7 @@ Geo geo(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny, in
 int64_t slot_doubles(int64_t lx, int64_t ly, const sk_kernel_config &c) {
   const int64_t L = std::max(lx, ly);
   const int64_t T = c.difference ? std::max<int64_t>(L - 1, 1) : std::max<int64_t>(L, 1);
-  // the row buffer of the wide (d >= 32) point-kernel evaluation, then the
+  // the row buffer of the wide (d > WIDE_D) point-kernel evaluation, then the
   // column accumulators of the long-row (more than 2 columns per thread) variant
   return L + 2 + std::max(c.n_levels - 1, 1) * T;
 }
@@ -1207,7 +1211,7 @@ int64_t redo_slot_doubles(int64_t lx, int64_t ly, int64_t d, const sk_kernel_con
 size_t long_row_smem(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   const int64_t L = std::max(lx, ly), T = c.difference ? L - 1 : L;
   const int64_t NV = std::max(c.n_levels - 1, 0), C = (T + RT - 1) / RT;
-  if (d >= 32 || L * d > YSTAGE_BYTES / 8 || C <= 2) return YSTAGE_BYTES;
+  if (d > WIDE_D || L * d > YSTAGE_BYTES / 8 || C <= 2) return YSTAGE_BYTES;
   const size_t need = (size_t)((((L * d + 1) & ~1ll) + NV * C * RT) * 8);
   return need <= (size_t)DYN_SMEM_MAX ? std::max<size_t>(YSTAGE_BYTES, need) : YSTAGE_BYTES;
 }
