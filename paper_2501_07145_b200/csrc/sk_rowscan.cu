@@ -1192,6 +1192,157 @@ Geo geo(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny, in
   return G;
 }
 
+// --- order 1, T' <= 256, d <= WIDE_D: one warp per pair ---------------------
+// The row scan above spends a block-wide scan (two barriers) per row on one
+// pair; here a warp owns the pair, lanes own C consecutive columns, and a row
+// costs the lanes' own point-kernel values (the previous row's kept in
+// registers, the column left of a lane's first one by shuffle), one warp scan
+// of the M-1 column-accumulator prefixes and the recursion — every state in
+// registers, the reference's arithmetic (kernels.py:144-201, :281).
+constexpr int WG_WARPS = 8;
+
+template <int C, int MB>
+__global__ void __launch_bounds__(32 * WG_WARPS) warp_gram_kernel(GramArgs A) {
+  const Geo &G = A.G;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, M = G.M, d = (int)G.d;
+  const bool diff = G.difference;
+  constexpr int VB = MB - 1;
+  const int64_t npairs = A.mode == 2 ? G.nx : A.rows * G.ny;
+  for (int64_t g = (int64_t)blockIdx.x * WG_WARPS + warp; g < npairs;
+       g += (int64_t)gridDim.x * WG_WARPS) {
+    int64_t i, j;
+    if (A.mode == 2) {
+      i = j = g;
+    } else {
+      i = A.row_begin + g / G.ny;
+      j = g % G.ny;
+      if (A.mode == 1 && j < i) continue;  // warp-uniform
+    }
+    const int64_t lxx = G.lx, lyy = A.mode == 2 ? G.lx : G.ly;
+    const double *xs = G.X + i * G.lx * d;
+    const double *ys = (A.mode == 2 ? G.X : G.Y) + j * lyy * d;
+    const int T1 = (int)(diff ? lxx - 1 : lxx), T2 = (int)(diff ? lyy - 1 : lyy);
+    double lsum[MB];
+#pragma unroll
+    for (int m = 0; m < MB; ++m) lsum[m] = 0.0;
+    if (M > 0 && T1 > 0 && T2 > 0) {
+      const int c0 = lane * C;  // own cells: columns c0 .. c0 + C - 1 of the increment grid
+      double ca[VB > 0 ? VB : 1][C];
+#pragma unroll
+      for (int m = 0; m < VB; ++m)
+#pragma unroll
+        for (int q = 0; q < C; ++q) ca[m][q] = 0.0;
+      // difference: point kernel G(r, c) at the own node columns c0+1 .. c0+C
+      // (gp: row r-1) and at column c0 (gl: from the left lane / lane 0 itself)
+      double gp[C], gpl = 0.0;
+      if (diff) {
+#pragma unroll
+        for (int q = 0; q < C; ++q)
+          gp[q] = c0 + q < T2 ? static_eval_f64(G.S, xs, ys + (c0 + q + 1) * d, d) : 0.0;
+        const double up = __shfl_up_sync(0xffffffffu, gp[C - 1], 1);
+        gpl = lane == 0 ? static_eval_f64(G.S, xs, ys, d) : up;
+      }
+      for (int r = 0; r < T1; ++r) {
+        double a[C];
+        if (diff) {
+          const double *xr = xs + (r + 1) * d;
+          double gc[C];
+#pragma unroll
+          for (int q = 0; q < C; ++q)
+            gc[q] = c0 + q < T2 ? static_eval_f64(G.S, xr, ys + (c0 + q + 1) * d, d) : 0.0;
+          const double up = __shfl_up_sync(0xffffffffu, gc[C - 1], 1);
+          const double gcl = lane == 0 ? static_eval_f64(G.S, xr, ys, d) : up;
+          // kernels.py:281: G[1:,1:] - G[:-1,1:] - G[1:,:-1] + G[:-1,:-1]
+#pragma unroll
+          for (int q = 0; q < C; ++q) {
+            const double g10 = q == 0 ? gcl : gc[q - 1], g00 = q == 0 ? gpl : gp[q - 1];
+            a[q] = c0 + q < T2 ? gc[q] - gp[q] - g10 + g00 : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < C; ++q) gp[q] = gc[q];
+          gpl = gcl;
+        } else {
+#pragma unroll
+          for (int q = 0; q < C; ++q)
+            a[q] = c0 + q < T2 ? static_eval_f64(G.S, xs + r * d, ys + (c0 + q) * d, d) : 0.0;
+        }
+        // exclusive prefix over columns of the column accumulators (old values)
+        double pre[VB > 0 ? VB : 1];
+#pragma unroll
+        for (int m = 0; m < VB; ++m) {
+          double t = 0.0;
+#pragma unroll
+          for (int q = 0; q < C; ++q) t += ca[m][q];
+          pre[m] = t;
+        }
+#pragma unroll
+        for (int m = 0; m < VB; ++m) {
+          if (m + 1 < M) {
+            double inc = pre[m];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const double u = __shfl_up_sync(0xffffffffu, inc, o);
+              if (lane >= o) inc += u;
+            }
+            pre[m] = inc - pre[m];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < C; ++q) {
+          double Rprev = a[q];  // R_1 (0 beyond the own cells)
+          lsum[0] += Rprev;
+#pragma unroll
+          for (int m = 1; m < MB; ++m) {
+            if (m < M) {
+              const double Rn = a[q] * pre[m - 1];  // R_{m+1} = A * S_m
+              lsum[m] += Rn;
+              pre[m - 1] += ca[m - 1][q];
+              ca[m - 1][q] += Rprev;
+              Rprev = Rn;
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MB; ++m) {
+      double v = lsum[m];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      lsum[m] = v;
+    }
+    if (lane == 0) {
+      double lv[MB + 1];
+      lv[0] = 1.0;
+#pragma unroll
+      for (int m = 0; m < MB; ++m) lv[m + 1] = m < M ? lsum[m] : 0.0;
+      if (A.mode == 2) {
+        for (int m = 0; m <= M; ++m) A.self_out[i * (M + 1) + m] = lv[m];
+      } else {
+        const bool sym = A.mode == 1;
+        const int64_t row = sym ? i : i - A.row_begin;
+        if (A.levels) {
+          for (int m = 0; m <= M; ++m) A.levels[(row * A.ldk + j) * (M + 1) + m] = lv[m];
+          if (sym && j != i)
+            for (int m = 0; m <= M; ++m) A.levels[(j * A.ldk + i) * (M + 1) + m] = lv[m];
+        }
+        if (A.K) {
+          const double v = finish_entry(lv, M, A.norm, A.diag_x ? A.diag_x + i * (M + 1) : nullptr,
+                                        A.diag_y ? A.diag_y + j * (M + 1) : nullptr);
+          A.K[row * A.ldk + j] = v;
+          if (sym && j != i) A.K[j * A.ldk + i] = v;
+        }
+      }
+    }
+  }
+}
+
+bool warp_gram_ok(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
+  const int p = std::max(1, std::min(c.order, std::max(c.n_levels, 1)));
+  const int64_t T = c.difference ? std::max(lx, ly) - 1 : std::max(lx, ly);
+  return p == 1 && c.n_levels >= 1 && c.n_levels <= 8 && d <= WIDE_D && T <= 256;
+}
+
 int64_t slot_doubles(int64_t lx, int64_t ly, const sk_kernel_config &c) {
   const int64_t L = std::max(lx, ly);
   const int64_t T = c.difference ? std::max<int64_t>(L - 1, 1) : std::max<int64_t>(L, 1);
@@ -1258,6 +1409,18 @@ int rowscan_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64
   const int64_t npairs = mode == 2 ? nx : A.rows * ny;
   if (npairs <= 0) return SK_OK;
   A.slot = slot_doubles(lx, mode == 2 ? lx : ly, c);
+  if (warp_gram_ok(lx, mode == 2 ? lx : ly, d, c)) {  // one warp per pair
+    const int64_t T = c.difference ? std::max(lx, mode == 2 ? lx : ly) - 1
+                                   : std::max(lx, mode == 2 ? lx : ly);
+    const int cc = T <= 32 ? 1 : (T <= 64 ? 2 : (T <= 128 ? 4 : 8));
+    const unsigned grid = (unsigned)std::min<int64_t>((npairs + WG_WARPS - 1) / WG_WARPS,
+                                                      (int64_t)sm_count() * 16);
+#define SK_WG(CC, MM) \
+    if (cc == CC && (MM == 4 ? c.n_levels <= 4 : c.n_levels > 4)) { \
+      warp_gram_kernel<CC, MM><<<grid, 32 * WG_WARPS, 0, st>>>(A); SK_CHECK_LAUNCH(); return SK_OK; }
+    SK_WG(1, 4) SK_WG(2, 4) SK_WG(4, 4) SK_WG(8, 4) SK_WG(1, 8) SK_WG(2, 8) SK_WG(4, 8) SK_WG(8, 8)
+#undef SK_WG
+  }
   if (wide_short(lx, mode == 2 ? lx : ly, d, c)) {  // block DGEMM + one-warp DP per pair
     const int64_t grid = std::min<int64_t>(npairs, (int64_t)sm_count());
     SK_CHECK_CUDA(cudaFuncSetAttribute(gram_kernel<true>,
