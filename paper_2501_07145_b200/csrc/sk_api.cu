@@ -71,9 +71,11 @@ int check_generic_limits(const sk_kernel_config &c) {
 
 // float64 path: the CTA-per-pair row-scan kernel at order 1 once rows have
 // >= 32 increments (below that most of a CTA would idle), else thread per pair
-bool use_rowscan(int64_t lx, int64_t ly, const sk_kernel_config &c) {
+// the row-scan kernels (warp-per-pair for short rows, CTA-per-pair beyond) or,
+// for short sequences outside the warp kernel's range, the generic kernel
+bool use_rowscan(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   const int64_t T2 = c.difference ? ly - 1 : ly;
-  return rowscan_supported(lx, ly, c) && T2 >= 32;
+  return rowscan_supported(lx, ly, c) && (T2 >= 32 || warp_gram_ok(lx, ly, d, c));
 }
 
 constexpr int64_t SELF64_MAX_L = 32;  // float64 general-order self levels up to this length
@@ -176,7 +178,7 @@ int sk_self_levels(const double *X, int64_t n, int64_t l, int64_t d,
     return rc;
   }
   if ((rc = check_generic_limits(*cfg))) return rc;
-  if (use_rowscan(l, l, *cfg))
+  if (use_rowscan(l, l, d, *cfg))
     return rowscan_gram(X, n, l, X, n, l, d, 2, *cfg, 0, n, nullptr, nullptr, nullptr, 0, nullptr,
                         out, workspace, workspace_bytes, st);
   return generic_self_levels(X, n, l, d, *cfg, out, workspace, workspace_bytes, st);
@@ -233,7 +235,7 @@ int sk_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64_t ny
     return rc;
   }
   if ((rc = check_generic_limits(*cfg))) return rc;
-  if (use_rowscan(lx, ly, *cfg))
+  if (use_rowscan(lx, ly, d, *cfg))
     return rowscan_gram(X, nx, lx, Y, ny, ly, d, symmetric ? 1 : 0, *cfg, row_begin, row_end,
                         diag_x, symmetric ? diag_x : diag_y, K, ldk, levels, nullptr, workspace,
                         workspace_bytes, st);

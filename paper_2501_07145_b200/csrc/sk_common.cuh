@@ -314,6 +314,7 @@ inline size_t k1buf_bytes(int64_t nx, int64_t ny, int /*norm*/) {
 // Order-1 float64 recursion with one CTA per pair (sk_rowscan.cu): the
 // float64 Gram / self levels for rows of >= 32 increments, and the FP32
 // certification's exact-level-1 pass + float64 redo of flagged entries.
+bool warp_gram_ok(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c);
 bool rowscan_supported(int64_t lx, int64_t ly, const sk_kernel_config &c);
 size_t rowscan_workspace_bytes(int64_t npairs, int64_t lx, int64_t ly, const sk_kernel_config &c);
 // mode 0 rect, 1 symmetric, 2 self levels (self_out)

@@ -1337,7 +1337,7 @@ __global__ void __launch_bounds__(32 * WG_WARPS) warp_gram_kernel(GramArgs A) {
   }
 }
 
-bool warp_gram_ok(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
+bool warp_ok(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
   const int p = std::max(1, std::min(c.order, std::max(c.n_levels, 1)));
   const int64_t T = c.difference ? std::max(lx, ly) - 1 : std::max(lx, ly);
   return p == 1 && c.n_levels >= 1 && c.n_levels <= 8 && d <= WIDE_D && T <= 256;
@@ -1375,6 +1375,10 @@ int64_t grid_for(int64_t work, int64_t slot) {
 
 }  // namespace rowscan
 
+bool warp_gram_ok(int64_t lx, int64_t ly, int64_t d, const sk_kernel_config &c) {
+  return rowscan::warp_ok(lx, ly, d, c);
+}
+
 bool rowscan_supported(int64_t lx, int64_t ly, const sk_kernel_config &c) {
   const int64_t L = std::max(lx, ly);
   const int64_t T = c.difference ? L - 1 : L;
@@ -1409,7 +1413,7 @@ int rowscan_gram(const double *X, int64_t nx, int64_t lx, const double *Y, int64
   const int64_t npairs = mode == 2 ? nx : A.rows * ny;
   if (npairs <= 0) return SK_OK;
   A.slot = slot_doubles(lx, mode == 2 ? lx : ly, c);
-  if (warp_gram_ok(lx, mode == 2 ? lx : ly, d, c)) {  // one warp per pair
+  if (warp_ok(lx, mode == 2 ? lx : ly, d, c)) {  // one warp per pair
     const int64_t T = c.difference ? std::max(lx, mode == 2 ? lx : ly) - 1
                                    : std::max(lx, mode == 2 ? lx : ly);
     const int cc = T <= 32 ? 1 : (T <= 64 ? 2 : (T <= 128 ? 4 : 8));
