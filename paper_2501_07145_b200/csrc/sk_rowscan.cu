@@ -1234,7 +1234,16 @@ __global__ void __launch_bounds__(32 * WG_WARPS) warp_gram_kernel(GramArgs A) {
         for (int q = 0; q < C; ++q) ca[m][q] = 0.0;
       // difference: point kernel G(r, c) at the own node columns c0+1 .. c0+C
       // (gp: row r-1) and at column c0 (gl: from the left lane / lane 0 itself)
-      double gp[C], gpl = 0.0;
+      double gp[C], gpl = 0.0, yyc[C];
+      const bool inner = G.S.kind == SK_LINEAR || G.S.kind == SK_POLYNOMIAL;
+#pragma unroll
+      for (int q = 0; q < C; ++q) {
+        yyc[q] = 0.0;
+        if (diff && !inner && c0 + q < T2) {
+          const double *yc = ys + (c0 + q + 1) * d;
+          for (int k = 0; k < d; ++k) yyc[q] = fma(yc[k], yc[k], yyc[q]);
+        }
+      }
       if (diff) {
 #pragma unroll
         for (int q = 0; q < C; ++q)
@@ -1247,9 +1256,22 @@ __global__ void __launch_bounds__(32 * WG_WARPS) warp_gram_kernel(GramArgs A) {
         if (diff) {
           const double *xr = xs + (r + 1) * d;
           double gc[C];
+          // the row's |x|^2 once, the columns' |y|^2 from the pair start: each
+          // cell is then one dot product (static_eval_f64's arithmetic)
+          double xx = 0.0;
+          if (!inner)
+            for (int k = 0; k < d; ++k) xx = fma(xr[k], xr[k], xx);
 #pragma unroll
-          for (int q = 0; q < C; ++q)
-            gc[q] = c0 + q < T2 ? static_eval_f64(G.S, xr, ys + (c0 + q + 1) * d, d) : 0.0;
+          for (int q = 0; q < C; ++q) {
+            if (c0 + q < T2) {
+              const double *yc = ys + (c0 + q + 1) * d;
+              double xy = 0.0;
+              for (int k = 0; k < d; ++k) xy = fma(xr[k], yc[k], xy);
+              gc[q] = inner ? static_from_inner(G.S, xy) : static_from_sq(G.S, xx + yyc[q] - 2.0 * xy);
+            } else {
+              gc[q] = 0.0;
+            }
+          }
           const double up = __shfl_up_sync(0xffffffffu, gc[C - 1], 1);
           const double gcl = lane == 0 ? static_eval_f64(G.S, xr, ys, d) : up;
           // kernels.py:281: G[1:,1:] - G[:-1,1:] - G[1:,:-1] + G[:-1,:-1]
